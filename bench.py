@@ -1,0 +1,396 @@
+"""Benchmark of the batch 2D tree SWDFT hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c4] [--impl ours|reference]
+
+One "step" = one pass of the hot path over the whole workload: the 2D SWDFT of
+the config's full input array, all P0 x P1 windows, output resident in HBM.
+Default workload: config 4 (4096x4096 f32 image-like array, 16x16 windows,
+4081x4081x16x16 complex64 = 34.2 GB), the config BASELINE.json quotes at
+1/2/4/8 GPUs.  Prints ONE JSON line (rank 0).
+
+  value      output coefficients / s, device-timed (CUDA events on the launching
+             stream), input resident in HBM, output preallocated; L2 flushed
+             (256 MiB write) between steps, outside the timed events
+  e2e        the same metric through the public API (tree_swdft_2d) from a
+             pinned host numpy-backed input to the full coefficient array in
+             pinned host memory: H2D + compute + D2H of every coefficient, per step
+  roofline   HBM bytes (algorithmic: output written + input read) / kernel time
+             vs the measured copy bandwidth in MEASURED_PEAKS.json
+  cpu_baseline  the C restatement of the reference (oracle/, all host threads)
+             on the first window rows of the same config (rank 0, N=1 only)
+
+N > 1 (torchrun, one process per GPU, NCCL): rank 0 holds the input in HBM;
+each step = scatter of input row strips with halos (NCCL send/recv from rank 0)
++ every rank's strip of the transform; time = max over ranks; strong scaling.
+
+--impl reference: times the CPU reference path (the oracle's C restatement of
+the reference's levels-outer tree, all host threads) on a bounded sample of the
+same workload, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "2D SWDFT output coeffs/sec & HBM write GB/s (% peak), 1/2/4/8 B200 vs CPU ref"
+UNIT = "coef/s"
+FALLBACK_HBM_GBS = 6650.0  # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
+
+
+def env_int(name, default):
+    v = os.environ.get(name)
+    return int(v) if v not in (None, "") else default
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy test)"
+    except (OSError, KeyError, ValueError):
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(config: str):
+    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        e = d.get(config)
+        return None if e is None else float(e["dram_bytes_per_launch"])
+    except (OSError, KeyError, ValueError):
+        return None
+
+
+class ClockSampler:
+    """Samples SM clock + throttle reasons with NVML while the timed region runs."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], 0, None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001 - NVML is optional evidence
+            self.nv = None
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:  # noqa: BLE001
+                pass
+            self._stop.wait(0.02)
+
+    def __enter__(self):
+        if self.nv is not None:
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join()
+
+    def summary(self):
+        if self.nv is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml_unavailable"]}
+        reasons = [n for bit, n in self.REASONS.items() if self.reasons & bit and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples)}
+
+
+def cpu_reference_rate(cfg, rows: int, reps: int, threads: int):
+    """Coefficients/s of the oracle's C restatement of the reference (levels-outer,
+    complex128, `threads` host threads) on window rows [0, rows) of the config."""
+    import oracle
+
+    oracle.build()
+    x = cfg.generate(rows=rows + cfg.n0 - 1)
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        out = oracle.tree2d(x, cfg.m0, cfg.m1, threads=threads, max_lattice_bytes=1 << 36)
+        times.append(time.perf_counter() - t0)
+    coefs = out.size
+    del out
+    return coefs / statistics.median(times), times, coefs
+
+
+def run_reference(args, cfg, rank):
+    if rank != 0:
+        return
+    threads = host_cores()
+    rows = args.ref_rows
+    for _ in range(args.warmup):
+        cpu_reference_rate(cfg, rows, 1, threads)
+    times = []
+    coefs = 0
+    for _ in range(args.steps):
+        rate, t, coefs = cpu_reference_rate(cfg, rows, 1, threads)
+        times.append(t[0])
+    tot = sum(times)
+    value = coefs * len(times) / tot
+    sample = (f"window rows [0,{rows}) of {cfg.name} ({coefs} coefficients, input rows "
+              f"[0,{rows + cfg.n0 - 1})), complex128, C restatement of the reference's "
+              f"levels-outer tree (oracle/swdft2d_oracle.c), {threads} threads on {cpu_model()}")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json recipe)",
+        "config": {"workload": cfg.name, "desc": cfg.desc, "sample_window_rows": rows},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def flush_l2(buf):
+    buf.fill_(1.0)
+
+
+def run_ours(args, cfg, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1707_08213_b200 import WindowSpec, tree_swdft_2d
+    from paper_1707_08213_b200 import _lib
+    from paper_1707_08213_b200.partition import strip_plan
+    from paper_1707_08213_b200.tree2d import _OUT_DTYPES, _precision_code, forward_into
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    spec = WindowSpec((cfg.m0, cfg.m1))
+    prec = _precision_code(cfg.precision, None)
+    odt = _OUT_DTYPES[prec]
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
+
+    x_np = cfg.generate() if rank == 0 else None
+    xdt = {"float32": torch.float32, "float64": torch.float64, "complex64": torch.complex64,
+           "complex128": torch.complex128}[cfg.dtype]
+    P0, P1, n0, n1 = cfg.P0, cfg.P1, cfg.n0, cfg.n1
+    plan = strip_plan(P0, cfg.m0, world)
+    a, b, rb, re = plan[rank]
+    out = torch.empty((b - a, P1, n0, n1), dtype=odt, device=dev)
+    if rank == 0:
+        x_full = torch.from_numpy(x_np).to(dev)
+    recv = None if rank == 0 else torch.empty((re - rb, cfg.N1), dtype=xdt, device=dev)
+
+    def step():
+        # scatter (N > 1): rank 0 -> every other rank, one batched NCCL group
+        if world > 1:
+            ops = []
+            if rank == 0:
+                for g, (_, _, gb, ge) in enumerate(plan):
+                    if g and ge > gb:
+                        ops.append(dist.P2POp(dist.isend, x_full[gb:ge], g))
+            elif re > rb:
+                ops.append(dist.P2POp(dist.irecv, recv, 0))
+            for req in dist.batch_isend_irecv(ops) if ops else []:
+                req.wait()
+        src = x_full[rb:re] if rank == 0 else recv
+        if b > a:
+            forward_into(src, cfg.m0, cfg.m1, out, prec=prec, stream=stream)
+
+    if world > 1:
+        dist.barrier()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    times = []
+    with ClockSampler(local_rank) as clk:
+        for _ in range(args.steps):
+            flush_l2(flush)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+    t_local = sum(times)
+    if world > 1:
+        tt = torch.tensor([t_local], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_job = float(tt.item())
+    else:
+        t_job = t_local
+    step_s = t_job / args.steps
+    value = cfg.coefficients / step_s
+    bytes_alg = cfg.algorithmic_bytes()
+
+    # kernel-only number for the roofline: the single K1 launch of one step (N=1)
+    kern_s = step_s
+    if world == 1:
+        kts = []
+        for _ in range(max(3, args.steps)):
+            flush_l2(flush)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            forward_into(x_full, cfg.m0, cfg.m1, out, prec=prec, stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            kts.append(e0.elapsed_time(e1) / 1e3)
+        kern_s = statistics.mean(kts)
+
+    peak, peak_src = measured_peak()
+    achieved = bytes_alg / kern_s / 1e9 if world == 1 else (
+        cfg.algorithmic_bytes(rows=b - a) / (t_local / args.steps) / 1e9)
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "f32" if prec == _lib.PREC_FP32 else "f64",
+        "data": "synthetic (seeded, BASELINE.json recipe; see paper_1707_08213_b200/workloads.py)",
+        "config": {"workload": cfg.name, "desc": cfg.desc, "N0": cfg.N0, "N1": cfg.N1,
+                   "window": [n0, n1], "coefficients": cfg.coefficients,
+                   "output_bytes": cfg.coefficients * cfg.out_bytes_per_coef,
+                   "l2": "256 MiB flush write between timed steps (outside the events); "
+                         "output >> L2 as well",
+                   "parallelism": f"strips{world}" if world > 1 else "single"},
+        "hbm_write_gbs": cfg.coefficients * cfg.out_bytes_per_coef / step_s / 1e9,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": ncu_traffic(cfg.name),
+                     "peak_source": peak_src,
+                     "bytes_per_launch": bytes_alg, "kernel_ms": kern_s * 1e3},
+        "clocks": clk.summary(),
+        "gpu_launches": args.steps,
+    }
+
+    # e2e through the public API from pinned host memory (N=1 only)
+    if world == 1 and not args.no_e2e:
+        line["e2e"] = e2e_host(args, cfg, x_np, dev, spec, odt, out)
+    if world == 1 and not args.no_cpu:
+        rate, t, coefs = cpu_reference_rate(cfg, args.ref_rows, 3, host_cores())
+        line["cpu_baseline"] = {
+            "value": rate, "unit": UNIT, "cores": host_cores(), "kind": "port",
+            "sample": f"window rows [0,{args.ref_rows}) of {cfg.name} ({coefs} coefficients), "
+                      f"median of 3, C restatement of the reference levels-outer tree "
+                      f"(oracle/swdft2d_oracle.c, complex128) on {cpu_model()}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def e2e_host(args, cfg, x_np, dev, spec, odt, out_dev):
+    """tree_swdft_2d(host x) -> device -> full coefficient array back in pinned host memory."""
+    import torch
+
+    from paper_1707_08213_b200 import tree_swdft_2d
+
+    x_pin = torch.from_numpy(x_np).pin_memory()
+    host_out = torch.empty(out_dev.shape, dtype=odt, pin_memory=True)
+    stream = torch.cuda.current_stream(dev)
+    times = []
+    for i in range(args.warmup + args.e2e_steps):
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        res = tree_swdft_2d(x_pin, spec, budget=1 << 62, device=dev, out=out_dev)
+        host_out.copy_(res.values, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if i >= args.warmup:
+            times.append(e0.elapsed_time(e1) / 1e3)
+    s = statistics.mean(times)
+    return {"value": cfg.coefficients / s, "unit": UNIT,
+            "h2d_bytes_per_step": int(x_pin.numel() * x_pin.element_size()),
+            "d2h_bytes_per_step": int(host_out.numel() * host_out.element_size()),
+            "ms_per_step": s * 1e3, "steps": len(times),
+            "path": "tree_swdft_2d(pinned host numpy input) + full D2H of the coefficients"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--ref-rows", type=int, default=128)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    from paper_1707_08213_b200.workloads import CONFIGS
+
+    cfg = CONFIGS[args.config]
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local_rank = env_int("LOCAL_RANK", 0)
+    if args.impl == "reference":
+        run_reference(args, cfg, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, cfg, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

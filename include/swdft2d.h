@@ -1,0 +1,126 @@
+/*
+ * swdft2d.h — C ABI of libswdft2d.so, the B200 (sm_100a) 2D tree sliding-window DFT.
+ *
+ * Drop-in boundary for the reference's batch 2D tree SWDFT,
+ *   swdft.tree2d.tree_swdft_2d(x, spec, loop_order, counter, budget, threads)
+ *   (/root/reference/pkg/src/swdft/tree2d.py:175-202).
+ * The reference has no FFI of its own (it is pure Python + numpy); these are the
+ * entry points its ctypes binding would call.  Plain
+ * pointers and sizes only: no torch types cross this boundary.
+ *
+ * Output convention (identical to the reference, core.py:258-285, tree2d.py:69):
+ *   out[p0, p1, k0, k1], p in window-START coordinates (P_i = N_i - n_i + 1),
+ *   = sum_{j0<n0, j1<n1} x[p0+j0, p1+j1] * exp(-2*pi*i*(j0*k0/n0 + j1*k1/n1)),
+ *   C-contiguous interleaved (re, im), natural-order k, k0 on axis 2.
+ *   Twiddles are core.make_twiddles (core.py:125-138), bitwise.
+ *
+ * Precision:
+ *   SWDFT2D_PREC_FP64 -> complex128 out, every tree node computed with the
+ *     reference's DAG and rounding order (core.py:223-246): bitwise equal to
+ *     tree_swdft_2d / oracle.swfft_2d.
+ *   SWDFT2D_PREC_FP32 -> complex64 out, fp32 arithmetic (FMA allowed);
+ *     BASELINE.json tolerance: max |err| / ||window||_2 <= 1e-4.
+ *
+ * Streams: every launch is stream-ordered on the caller's cudaStream_t (passed
+ * as void*); the library allocates no device memory per call (the K0 twiddle
+ * table cache is allocated once per device and freed by swdft2d_shutdown).
+ * Errors: functions return SWDFT2D_OK (0) or a negative code; the message of
+ * the last error on the calling thread is swdft2d_last_error().
+ */
+#ifndef SWDFT2D_H_
+#define SWDFT2D_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SWDFT2D_ABI_VERSION 1
+
+/* status codes; the Python wrapper maps them onto the reference's exception
+ * classes (core.py:23-56). */
+#define SWDFT2D_OK 0
+#define SWDFT2D_E_INVALID_ARG (-1)       /* ValueError                    */
+#define SWDFT2D_E_SHAPE (-2)             /* core.ShapeError               */
+#define SWDFT2D_E_WINDOW_TOO_LARGE (-3)  /* core.WindowTooLargeError      */
+#define SWDFT2D_E_INVALID_WINDOW (-4)    /* core.InvalidWindowError       */
+#define SWDFT2D_E_UNSUPPORTED (-6)       /* shape outside the CUDA paths  */
+#define SWDFT2D_E_CUDA (-7)              /* CUDA runtime / launch failure */
+#define SWDFT2D_E_NOMEM (-8)             /* device allocation failed      */
+
+/* element type of x */
+#define SWDFT2D_IN_F32 0
+#define SWDFT2D_IN_F64 1
+#define SWDFT2D_IN_C64 2
+#define SWDFT2D_IN_C128 3
+
+/* arithmetic precision == output element type */
+#define SWDFT2D_PREC_FP32 0 /* complex64 out  */
+#define SWDFT2D_PREC_FP64 1 /* complex128 out */
+
+/* kernel selection for swdft2d_forward */
+#define SWDFT2D_KERNEL_AUTO 0   /* K1 when instantiated for (m0, m1), else K0 */
+#define SWDFT2D_KERNEL_STREAM 1 /* K1: fused row-streaming tree kernel          */
+#define SWDFT2D_KERNEL_WINDOW 2 /* K0: per-(window, k1) DAG kernel (bring-up)   */
+
+/* Largest window exponent handled by K1 / by K0. */
+#define SWDFT2D_K1_MAX_M 6
+#define SWDFT2D_K0_MAX_M 10
+
+int swdft2d_abi_version(void);
+
+/* Message of the last failing call on this thread ("" if none). */
+const char *swdft2d_last_error(void);
+
+/* core.WindowSpec.check_fits (core.py:116-122) and P_i = N_i - n_i + 1.
+ * Returns SWDFT2D_E_WINDOW_TOO_LARGE when n_i > N_i. */
+int swdft2d_output_shape(int64_t N0, int64_t N1, int m0, int m1, int64_t *P0, int64_t *P1);
+
+/* core.lattice_bytes + core.output_bytes (core.py:363-381): the reference's
+ * memory accounting at 16 B per complex, used by the wrapper's budget check
+ * (tree2d.py:195-196). */
+int swdft2d_reference_bytes(int64_t N0, int64_t N1, int m0, int m1, int64_t *lattice_bytes,
+                            int64_t *output_bytes);
+
+/* core.make_twiddles(n) (core.py:125-138) into out[2*n] as interleaved float64
+ * (re, im).  Same libm formula, bitwise equal to numpy's table on x86-64 glibc. */
+int swdft2d_twiddles(int n, double *out_interleaved);
+
+/*
+ * Batch 2D tree SWDFT of window rows [p0_begin, p0_end) — replaces the compute of
+ * tree_swdft_2d (tree2d.py:197-202: _levels_outer + coefficients() + normalize).
+ *   x        device pointer, N0 x N1 elements of in_dtype, row stride ld_x elements
+ *   m0, m1   window exponents (n_i = 2^m_i), as WindowSpec.exponents
+ *   prec     SWDFT2D_PREC_FP32 / SWDFT2D_PREC_FP64
+ *   scale    normalization factor (core.normalization_factor); 1.0 = mode "none"
+ *   out      device pointer, (p0_end - p0_begin) x P1 x n0 x n1 complex of prec,
+ *            C-contiguous; row p0 of the full output lands at out row p0 - p0_begin
+ *   kernel   SWDFT2D_KERNEL_*
+ *   stream   cudaStream_t (NULL = legacy default stream)
+ * Reads only input rows [p0_begin, p0_end + n0 - 1), so a strip of x (with its
+ * n0-1 halo rows) can be passed with p0 relative to the strip.
+ */
+int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t ld_x, int m0,
+                    int m1, int prec, double scale, int64_t p0_begin, int64_t p0_end, void *out,
+                    int kernel, void *stream);
+
+/* Whether K1 is instantiated for (m0, m1, prec): 1 yes, 0 no. */
+int swdft2d_has_stream_kernel(int m0, int m1, int prec);
+
+/*
+ * Window-row strip partition for world ranks (single box):
+ * rank g of G gets window rows [floor(P0*g/G), floor(P0*(g+1)/G)) and input rows
+ * [p0_begin, p0_end + n0 - 1).  range = {p0_begin, p0_end, row_begin, row_end}.
+ * Empty ranges are legal (P0 < G).
+ */
+int swdft2d_strip_range(int64_t P0, int m0, int rank, int world, int64_t range[4]);
+
+/* Frees cached per-device state (twiddle tables).  Safe to call twice. */
+int swdft2d_shutdown(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SWDFT2D_H_ */

@@ -1,0 +1,116 @@
+"""ctypes binding of libswdft2d.so (include/swdft2d.h).
+
+The library is built in-tree (``python -m paper_1707_08213_b200.build``).  There
+is no CPU fallback: if the library is missing or cannot be loaded, importing
+the compute entry points raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+from . import core
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.environ.get("SWDFT2D_LIB", os.path.join(_HERE, "libswdft2d.so"))
+
+ABI_VERSION = 1
+
+OK = 0
+E_INVALID_ARG = -1
+E_SHAPE = -2
+E_WINDOW_TOO_LARGE = -3
+E_INVALID_WINDOW = -4
+E_UNSUPPORTED = -6
+E_CUDA = -7
+E_NOMEM = -8
+
+IN_F32, IN_F64, IN_C64, IN_C128 = 0, 1, 2, 3
+PREC_FP32, PREC_FP64 = 0, 1
+KERNEL_AUTO, KERNEL_STREAM, KERNEL_WINDOW = 0, 1, 2
+KERNELS = {"auto": KERNEL_AUTO, "stream": KERNEL_STREAM, "window": KERNEL_WINDOW}
+
+# every symbol include/swdft2d.h declares: name -> (restype, argtypes)
+_i64, _int, _dbl, _vp = ctypes.c_int64, ctypes.c_int, ctypes.c_double, ctypes.c_void_p
+_pi64 = ctypes.POINTER(ctypes.c_int64)
+SIGNATURES = {
+    "swdft2d_abi_version": (_int, []),
+    "swdft2d_last_error": (ctypes.c_char_p, []),
+    "swdft2d_output_shape": (_int, [_i64, _i64, _int, _int, _pi64, _pi64]),
+    "swdft2d_reference_bytes": (_int, [_i64, _i64, _int, _int, _pi64, _pi64]),
+    "swdft2d_twiddles": (_int, [_int, ctypes.POINTER(ctypes.c_double)]),
+    "swdft2d_forward": (_int, [_vp, _int, _i64, _i64, _i64, _int, _int, _int, _dbl, _i64, _i64,
+                               _vp, _int, _vp]),
+    "swdft2d_has_stream_kernel": (_int, [_int, _int, _int]),
+    "swdft2d_strip_range": (_int, [_i64, _int, _int, _int, _pi64]),
+    "swdft2d_shutdown": (_int, []),
+}
+
+_lib = None
+
+
+def load() -> ctypes.CDLL:
+    """Load libswdft2d.so (once).  Raises ImportError when it is absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} not found: build it with `python -m paper_1707_08213_b200.build` "
+            "(there is no CPU fallback for the SWDFT path)")
+    lib = ctypes.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    v = lib.swdft2d_abi_version()
+    if v != ABI_VERSION:
+        raise ImportError(f"libswdft2d.so ABI {v} != expected {ABI_VERSION}")
+    _lib = lib
+    return lib
+
+
+def last_error() -> str:
+    return load().swdft2d_last_error().decode(errors="replace")
+
+
+def check(rc: int) -> None:
+    """Map a status code onto the reference's exception classes (core.py:23-56)."""
+    if rc == OK:
+        return
+    msg = last_error()
+    if rc == E_SHAPE:
+        raise core.ShapeError(msg)
+    if rc == E_WINDOW_TOO_LARGE:
+        raise core.WindowTooLargeError(msg)
+    if rc == E_INVALID_WINDOW:
+        raise core.InvalidWindowError(msg)
+    if rc == E_INVALID_ARG:
+        raise ValueError(msg)
+    if rc == E_UNSUPPORTED:
+        raise core.UnsupportedError(msg)
+    if rc in (E_CUDA, E_NOMEM):
+        raise core.DeviceError(msg)
+    raise core.SwdftError(f"libswdft2d error {rc}: {msg}")
+
+
+def strip_range(P0: int, m0: int, rank: int, world: int):
+    """(p0_begin, p0_end, row_begin, row_end) of one rank (swdft2d_strip_range)."""
+    buf = (ctypes.c_int64 * 4)()
+    check(load().swdft2d_strip_range(P0, m0, rank, world, buf))
+    return tuple(int(v) for v in buf)
+
+
+def twiddles(n: int):
+    import numpy as np
+
+    out = np.empty(2 * n, dtype=np.float64)
+    check(load().swdft2d_twiddles(n, out.ctypes.data_as(ctypes.POINTER(ctypes.c_double))))
+    t = np.empty(n, dtype=np.complex128)
+    t.real = out[0::2]
+    t.imag = out[1::2]
+    return t
+
+
+def has_stream_kernel(m0: int, m1: int, prec: int) -> bool:
+    return bool(load().swdft2d_has_stream_kernel(m0, m1, prec))

@@ -1,0 +1,349 @@
+// abi.cu — extern "C" boundary of libswdft2d.so (declared in include/swdft2d.h).
+//
+// Mirrors the validation, accounting and dispatch the reference does around its
+// compute (tree2d.py:175-202, core.py:116-122, 363-388) and launches K1 (fused
+// streaming tree, k1_stream.cuh) or K0 (per-window DAG, k0_window.cu) on the
+// caller's stream.  No torch types, no host threads, no per-call device
+// allocation.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <utility>
+
+#include "../../include/swdft2d.h"
+#include "swdft2d_internal.h"
+
+namespace swdft2d {
+
+void k1_register_m0_0();
+void k1_register_m0_1();
+void k1_register_m0_2();
+void k1_register_m0_3();
+void k1_register_m0_4();
+void k1_register_m0_5();
+void k1_register_m0_6();
+
+static thread_local std::string g_last_error;
+
+static int fail(int code, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+static int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
+// ---- K1 registry ---------------------------------------------------------
+static const K1Info *g_k1[SWDFT2D_K1_MAX_M + 1][SWDFT2D_K1_MAX_M + 1][2];
+
+void register_k1(const K1Info *info) { g_k1[info->m0][info->m1][info->prec] = info; }
+
+static void ensure_registered() {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        k1_register_m0_0();
+        k1_register_m0_1();
+        k1_register_m0_2();
+        k1_register_m0_3();
+        k1_register_m0_4();
+        k1_register_m0_5();
+        k1_register_m0_6();
+    });
+}
+
+const K1Info *find_k1(int m0, int m1, int prec) {
+    ensure_registered();
+    if (m0 < 0 || m1 < 0 || m0 > SWDFT2D_K1_MAX_M || m1 > SWDFT2D_K1_MAX_M || prec < 0 || prec > 1)
+        return nullptr;
+    return g_k1[m0][m1][prec];
+}
+
+// ---- per-device state ----------------------------------------------------
+struct DeviceState {
+    int sms = 0;
+    void *k0_tw64 = nullptr;  // double2[K0_TW_N]
+    void *k0_tw32 = nullptr;  // float2[K0_TW_N]
+    std::map<const void *, int> occupancy;  // K1 function -> CTAs per SM
+};
+static std::mutex g_mu;
+static std::map<int, DeviceState> g_dev;
+
+// core.make_twiddles (core.py:134-137): ang = j * fl(2*pi/n); (cos, -sin).
+static void host_twiddles(int n, double *re, double *im) {
+    const double step = (2.0 * 3.141592653589793) / (double)n;
+    for (int j = 0; j < n; ++j) {
+        const double ang = (double)j * step;
+        re[j] = std::cos(ang);
+        im[j] = -std::sin(ang);
+    }
+}
+
+static int device_state(DeviceState **out) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return fail(SWDFT2D_E_CUDA, "cudaGetDevice: %s", cudaGetErrorString(e));
+    std::lock_guard<std::mutex> lk(g_mu);
+    DeviceState &st = g_dev[dev];
+    if (st.sms == 0) {
+        e = cudaDeviceGetAttribute(&st.sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e != cudaSuccess)
+            return fail(SWDFT2D_E_CUDA, "cudaDeviceGetAttribute: %s", cudaGetErrorString(e));
+    }
+    *out = &st;
+    return SWDFT2D_OK;
+}
+
+static int k0_tables(DeviceState *st, const void **tw64, const void **tw32) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (!st->k0_tw64) {
+        static double re[K0_TW_N], im[K0_TW_N];
+        static double2 h64[K0_TW_N];
+        static float2 h32[K0_TW_N];
+        host_twiddles(K0_TW_N, re, im);
+        for (int i = 0; i < K0_TW_N; ++i) {
+            h64[i] = make_double2(re[i], im[i]);
+            h32[i] = make_float2((float)re[i], (float)im[i]);
+        }
+        cudaError_t e = cudaMalloc(&st->k0_tw64, sizeof h64);
+        if (e == cudaSuccess) e = cudaMalloc(&st->k0_tw32, sizeof h32);
+        if (e == cudaSuccess) e = cudaMemcpy(st->k0_tw64, h64, sizeof h64, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMemcpy(st->k0_tw32, h32, sizeof h32, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) {
+            cudaFree(st->k0_tw64);
+            cudaFree(st->k0_tw32);
+            st->k0_tw64 = st->k0_tw32 = nullptr;
+            return fail(SWDFT2D_E_NOMEM, "twiddle table: %s", cudaGetErrorString(e));
+        }
+    }
+    *tw64 = st->k0_tw64;
+    *tw32 = st->k0_tw32;
+    return SWDFT2D_OK;
+}
+
+static int k1_occupancy(DeviceState *st, const K1Info *info, int *occ) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = st->occupancy.find(info->func);
+    if (it != st->occupancy.end()) {
+        *occ = it->second;
+        return SWDFT2D_OK;
+    }
+    cudaError_t e = cudaSuccess;
+    if (info->smem_bytes > 48 * 1024)
+        e = cudaFuncSetAttribute(info->func, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)info->smem_bytes);
+    int n = 0;
+    if (e == cudaSuccess)
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, info->func, info->threads,
+                                                          info->smem_bytes);
+    if (e != cudaSuccess)
+        return fail(SWDFT2D_E_CUDA, "K1 occupancy (m0=%d m1=%d): %s", info->m0, info->m1,
+                    cudaGetErrorString(e));
+    if (n < 1)
+        return fail(SWDFT2D_E_UNSUPPORTED, "K1 (m0=%d m1=%d) cannot be resident (smem %zu B)",
+                    info->m0, info->m1, info->smem_bytes);
+    st->occupancy[info->func] = n;
+    *occ = n;
+    return SWDFT2D_OK;
+}
+
+// Row-chunk size for K1 tiles: minimise (waves x rows per tile incl. the n0-1
+// warm-up rows); an under-filled single wave is charged as if it ran at the
+// fraction of the slots it occupies.
+static int64_t k1_rows_per_tile(int64_t rows, int64_t CB, int64_t slots, int n0) {
+    int64_t best_rch = rows;
+    double best = 1e300;
+    const int64_t rc_max = rows < 8192 ? rows : 8192;
+    for (int64_t rc = 1; rc <= rc_max; ++rc) {
+        const int64_t rch = (rows + rc - 1) / rc;
+        const int64_t rca = (rows + rch - 1) / rch;
+        const int64_t tiles = CB * rca;
+        const double per = (double)(rch + n0 - 1);
+        double cost;
+        if (tiles >= slots) cost = (double)((tiles + slots - 1) / slots) * per;
+        else cost = per * (double)slots / (double)tiles;
+        if (cost < best * 0.999) {
+            best = cost;
+            best_rch = rch;
+        }
+    }
+    return best_rch;
+}
+
+}  // namespace swdft2d
+
+using namespace swdft2d;
+
+extern "C" {
+
+int swdft2d_abi_version(void) { return SWDFT2D_ABI_VERSION; }
+
+const char *swdft2d_last_error(void) { return g_last_error.c_str(); }
+
+int swdft2d_output_shape(int64_t N0, int64_t N1, int m0, int m1, int64_t *P0, int64_t *P1) {
+    if (m0 < 0 || m1 < 0) return fail(SWDFT2D_E_INVALID_WINDOW, "window exponents must be non-negative");
+    if (m0 > 62 || m1 > 62) return fail(SWDFT2D_E_INVALID_WINDOW, "window exponent too large");
+    const int64_t n0 = (int64_t)1 << m0, n1 = (int64_t)1 << m1;
+    if (n0 > N0)
+        return fail(SWDFT2D_E_WINDOW_TOO_LARGE, "window size %lld exceeds extent %lld in dimension 0",
+                    (long long)n0, (long long)N0);
+    if (n1 > N1)
+        return fail(SWDFT2D_E_WINDOW_TOO_LARGE, "window size %lld exceeds extent %lld in dimension 1",
+                    (long long)n1, (long long)N1);
+    if (P0) *P0 = N0 - n0 + 1;
+    if (P1) *P1 = N1 - n1 + 1;
+    return SWDFT2D_OK;
+}
+
+int swdft2d_reference_bytes(int64_t N0, int64_t N1, int m0, int m1, int64_t *lattice_bytes,
+                            int64_t *output_bytes) {
+    int64_t P0 = 0, P1 = 0;
+    int rc = swdft2d_output_shape(N0, N1, m0, m1, &P0, &P1);
+    if (rc) return rc;
+    // 16 B per complex (core.COMPLEX_BYTES, core.py:17); saturate instead of overflowing.
+    const long double win = std::ldexp(1.0L, m0 + m1);
+    const long double lat = 2.0L * (long double)N0 * (long double)N1 * win * 16.0L;
+    const long double outb = (long double)P0 * (long double)P1 * win * 16.0L;
+    const long double lim = 9.2e18L;
+    if (lattice_bytes) *lattice_bytes = lat > lim ? INT64_MAX : (int64_t)lat;
+    if (output_bytes) *output_bytes = outb > lim ? INT64_MAX : (int64_t)outb;
+    return SWDFT2D_OK;
+}
+
+int swdft2d_twiddles(int n, double *out) {
+    if (n < 1 || (n & (n - 1)) != 0)
+        return fail(SWDFT2D_E_INVALID_WINDOW, "twiddle table size %d is not a power of two", n);
+    if (!out) return fail(SWDFT2D_E_INVALID_ARG, "null output");
+    const double step = (2.0 * 3.141592653589793) / (double)n;
+    for (int j = 0; j < n; ++j) {
+        const double ang = (double)j * step;
+        out[2 * j] = std::cos(ang);
+        out[2 * j + 1] = -std::sin(ang);
+    }
+    return SWDFT2D_OK;
+}
+
+int swdft2d_has_stream_kernel(int m0, int m1, int prec) { return find_k1(m0, m1, prec) ? 1 : 0; }
+
+int swdft2d_strip_range(int64_t P0, int m0, int rank, int world, int64_t range[4]) {
+    if (world < 1 || rank < 0 || rank >= world || P0 < 0 || m0 < 0 || m0 > 62 || !range)
+        return fail(SWDFT2D_E_INVALID_ARG, "bad strip request (P0=%lld rank=%d world=%d)",
+                    (long long)P0, rank, world);
+    const int64_t n0 = (int64_t)1 << m0;
+    // floor(P0*g/G) without overflow for P0 < 2^62 / world
+    const int64_t a = (int64_t)(((__int128)P0 * rank) / world);
+    const int64_t b = (int64_t)(((__int128)P0 * (rank + 1)) / world);
+    range[0] = a;
+    range[1] = b;
+    range[2] = a;
+    range[3] = b > a ? b + n0 - 1 : a;
+    return SWDFT2D_OK;
+}
+
+int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t ld_x, int m0,
+                    int m1, int prec, double scale, int64_t p0_begin, int64_t p0_end, void *out,
+                    int kernel, void *stream) {
+    if (in_dtype < SWDFT2D_IN_F32 || in_dtype > SWDFT2D_IN_C128)
+        return fail(SWDFT2D_E_INVALID_ARG, "unknown input dtype code %d", in_dtype);
+    if (prec != SWDFT2D_PREC_FP32 && prec != SWDFT2D_PREC_FP64)
+        return fail(SWDFT2D_E_INVALID_ARG, "unknown precision code %d", prec);
+    if (N0 < 1 || N1 < 1) return fail(SWDFT2D_E_SHAPE, "empty input (%lld x %lld)", (long long)N0, (long long)N1);
+    if (ld_x < N1) return fail(SWDFT2D_E_INVALID_ARG, "ld_x %lld < N1 %lld", (long long)ld_x, (long long)N1);
+    int64_t P0 = 0, P1 = 0;
+    int rc = swdft2d_output_shape(N0, N1, m0, m1, &P0, &P1);
+    if (rc) return rc;
+    if (p0_begin < 0 || p0_end > P0 || p0_begin > p0_end)
+        return fail(SWDFT2D_E_INVALID_ARG, "window rows [%lld, %lld) outside [0, %lld)",
+                    (long long)p0_begin, (long long)p0_end, (long long)P0);
+    if (p0_begin == p0_end) return SWDFT2D_OK;
+    if (!x || !out) return fail(SWDFT2D_E_INVALID_ARG, "null device pointer");
+    if (kernel < SWDFT2D_KERNEL_AUTO || kernel > SWDFT2D_KERNEL_WINDOW)
+        return fail(SWDFT2D_E_INVALID_ARG, "unknown kernel code %d", kernel);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    DeviceState *ds = nullptr;
+    if ((rc = device_state(&ds))) return rc;
+    const int n0 = 1 << m0;
+    const bool apply = !(scale == 1.0);
+
+    const K1Info *k1 = find_k1(m0, m1, prec);
+    if (kernel == SWDFT2D_KERNEL_STREAM && !k1)
+        return fail(SWDFT2D_E_UNSUPPORTED, "no K1 instantiation for m0=%d m1=%d prec=%d", m0, m1, prec);
+    if (kernel != SWDFT2D_KERNEL_WINDOW && k1) {
+        int occ = 0;
+        if ((rc = k1_occupancy(ds, k1, &occ))) return rc;
+        K1Params P;
+        std::memset(&P, 0, sizeof P);
+        P.x = x;
+        P.in_dtype = in_dtype;
+        P.apply_scale = apply ? 1 : 0;
+        P.N0 = N0;
+        P.N1 = N1;
+        P.ldx = ld_x;
+        P.p0_begin = p0_begin;
+        P.p0_end = p0_end;
+        P.P1 = P1;
+        P.out = out;
+        P.scale = scale;
+        P.CB = (P1 + k1->tp1 - 1) / k1->tp1;
+        const int64_t rows = p0_end - p0_begin;
+        const int64_t slots = (int64_t)ds->sms * occ;
+        P.RCH = k1_rows_per_tile(rows, P.CB, slots, n0);
+        P.ntiles = P.CB * ((rows + P.RCH - 1) / P.RCH);
+        double re[K1_TW_N], im[K1_TW_N];
+        host_twiddles(K1_TW_N, re, im);
+        for (int i = 0; i < K1_TW_N; ++i) P.tw[i] = make_double2(re[i], im[i]);
+        const int64_t grid = P.ntiles < slots ? P.ntiles : slots;
+        k1->launch(P, (int)grid, st);
+    } else {
+        if (m0 > SWDFT2D_K0_MAX_M || m1 > SWDFT2D_K0_MAX_M)
+            return fail(SWDFT2D_E_UNSUPPORTED, "window 2^%d x 2^%d exceeds the CUDA paths (max 2^%d)",
+                        m0, m1, SWDFT2D_K0_MAX_M);
+        const void *tw64 = nullptr, *tw32 = nullptr;
+        if ((rc = k0_tables(ds, &tw64, &tw32))) return rc;
+        K0Params P;
+        std::memset(&P, 0, sizeof P);
+        P.x = x;
+        P.in_dtype = in_dtype;
+        P.m0 = m0;
+        P.m1 = m1;
+        P.apply_scale = apply ? 1 : 0;
+        P.ldx = ld_x;
+        P.p0_begin = p0_begin;
+        P.p0_end = p0_end;
+        P.P1 = P1;
+        P.out = out;
+        P.scale = scale;
+        P.tw = prec == SWDFT2D_PREC_FP64 ? tw64 : tw32;
+        P.tw_n = K0_TW_N;
+        if (launch_k0(P, prec, st))
+            return fail(SWDFT2D_E_UNSUPPORTED, "K0 grid too large for %lld x %lld outputs",
+                        (long long)(p0_end - p0_begin), (long long)P1);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(SWDFT2D_E_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+    return SWDFT2D_OK;
+}
+
+int swdft2d_shutdown(void) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    int cur = 0;
+    cudaGetDevice(&cur);
+    for (auto &kv : g_dev) {
+        if (kv.second.k0_tw64 || kv.second.k0_tw32) {
+            cudaSetDevice(kv.first);
+            cudaFree(kv.second.k0_tw64);
+            cudaFree(kv.second.k0_tw32);
+        }
+    }
+    g_dev.clear();
+    cudaSetDevice(cur);
+    return SWDFT2D_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,277 @@
+// k1_stream.cuh — K1, the fused row-streaming 2D tree SWDFT kernel for sm_100a.
+//
+// The reference computes the tree levels-outer over a double-buffered
+// [N0, N1, n0, n1] lattice (tree2d.py:30-129): every level is a full pass over
+// HBM-sized slabs.  The tree factorises exactly:
+//   stage R  (tree levels 1..m1, dim 1, row_level_step tree2d.py:72-93)
+//            Z[r, p1, k1] = n1-point DIT transform of x[r, p1 : p1+n1]
+//   stage C  (tree levels m1+1..m1+m0, dim 0, col_level_step tree2d.py:96-120)
+//            a[p0, p1, k0, k1] = 1D tree along rows of the column Z[:, p1, k1]
+// K1 streams each CTA down a strip of input rows, so no tree level ever
+// reaches HBM: only the final coefficients are written (the HBM-write
+// roofline of the path).
+//
+// CTA = TP1 consecutive window columns x all n1 frequencies k1 x J "k0
+// residue groups".  Thread (k1, j, pos) owns column (pos, k1) and the output
+// frequencies k0 = j + J*u.  Work is done in batches of NB input rows:
+//   1. stage R: the warps split the NB x TP1 row transforms; each transform
+//      is an n1-point radix-2 DIT on G = min(n1, 32) lanes (V = n1/G values
+//      per lane) with warp shuffles for the level exchanges, written into a
+//      shared-memory ring Z[D][TP1][n1] (D >= n0 rows of history).
+//   2. __syncthreads
+//   3. stage C, per row: the thread rebuilds the level-Q node j of its column
+//      tree from J ring rows (2^Q - 1 butterflies, the reference DAG), then
+//      advances levels Q+1..m0 with the tree's reuse along p0: the level l-1
+//      node of the tree s_l rows back (tree2d.py:110) comes from a register
+//      ring, so each row costs 2(n0/J - 1) butterflies per thread.  The n0/J
+//      finished coefficients are written with streaming (evict-first) stores;
+//      consecutive lanes hold consecutive k1, so each warp store is a
+//      contiguous 256-byte (complex64) run of the [P0, P1, n0, n1] output.
+//   4. __syncthreads (ring slots are recycled by the next batch's stage R)
+//
+// EXACT (fp64) instantiations use the reference's operand roles and rounding
+// order for every node (core.py:238-245 via bfly_exact, the node's own
+// twiddle Omega[i*s] — no +-w pair symmetry, which is not bitwise,
+// SURVEY.md App. A #3), so they reproduce tree_swdft_2d bit for bit.  The fp32
+// instantiations use FMAs and the pair symmetry w[i + L/2] = -w[i].
+#pragma once
+
+#include <type_traits>
+
+#include "swdft2d_device.cuh"
+#include "swdft2d_internal.h"
+
+namespace swdft2d {
+
+constexpr int cmax(int a, int b) { return a > b ? a : b; }
+constexpr int cmin(int a, int b) { return a < b ? a : b; }
+constexpr int pow2ceil(int v) {
+    int p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+template <int M0, int M1, int Q, int TP1> struct K1Shape {
+    static constexpr int n0 = 1 << M0, n1 = 1 << M1, J = 1 << Q;
+    static constexpr int NT = n1 * J * TP1;               // threads per CTA
+    static constexpr int WARPS = NT / 32;
+    static constexpr int NB = cmax(n0 / J, 4);            // rows per batch
+    static constexpr int D = pow2ceil(n0 - n0 / J + NB);  // Z ring depth (rows)
+    static constexpr int G = cmin(n1, 32);                // lanes per row transform
+    static constexpr int V = n1 / G;                      // values per lane
+    static constexpr int GW = 32 / G;                     // transforms per warp task
+    static constexpr int TPR = (TP1 + GW - 1) / GW;       // warp tasks per row
+    static constexpr int TASKS = NB * TPR;
+    static constexpr int TPW = (TASKS + WARPS - 1) / WARPS;
+    static constexpr int NMAX = cmax(n0, n1);
+    static constexpr int RING = cmax((M0 - Q) * (n0 / (2 * J)), 1);  // register ring, complex
+    static constexpr int OUTS = n0 / J;                   // coefficients per thread per row
+    static_assert(Q <= M0, "J must divide n0");
+    static_assert(NT % 32 == 0 && NT <= 1024, "CTA size must be a warp multiple <= 1024");
+};
+
+template <typename T, int M0, int M1, int Q, int TP1>
+constexpr size_t k1_smem_bytes() {
+    using S = K1Shape<M0, M1, Q, TP1>;
+    return sizeof(cplx<T>) * ((size_t)S::D * TP1 * S::n1 + S::NMAX);
+}
+
+template <typename T, int M0, int M1, int Q, int TP1, bool EXACT>
+__global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1>::NT)
+    k1_stream_kernel(const __grid_constant__ K1Params P) {
+    using S = K1Shape<M0, M1, Q, TP1>;
+    using C = cplx<T>;
+    constexpr int n0 = S::n0, n1 = S::n1, J = S::J, NB = S::NB, D = S::D;
+    constexpr int G = S::G, V = S::V, GW = S::GW, TPR = S::TPR, NMAX = S::NMAX;
+    constexpr int ST0 = NMAX / n0, ST1 = NMAX / n1;  // table strides (exact, App. A #4)
+
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    C *ring = reinterpret_cast<C *>(smem_raw);  // [D][TP1][n1]
+    C *tw = ring + D * TP1 * n1;                // make_twiddles(NMAX)
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < NMAX; i += S::NT) {
+        const double2 w = P.tw[i * (K1_TW_N / NMAX)];
+        tw[i] = mk<T>((T)w.x, (T)w.y);
+    }
+    __syncthreads();
+
+    // stage C identity: column (pos, k1), output residue j
+    const int k1 = tid % n1, j = (tid / n1) % J, pos = tid / (n1 * J);
+    // stage R identity: lane lam of transform group gam
+    const int gam = lane / G, lam = lane % G;
+
+    C rring[S::RING];  // level l-1 nodes of the last s_l rows, levels Q+1..m0
+    C cur[S::OUTS];
+#pragma unroll
+    for (int q = 0; q < S::RING; ++q) rring[q] = mk<T>(0, 0);
+
+    for (int64_t tile = blockIdx.x; tile < P.ntiles; tile += gridDim.x) {
+        const int64_t cb = tile % P.CB, rc = tile / P.CB;
+        const int64_t pbase = cb * TP1;
+        const int64_t r0 = P.p0_begin + rc * P.RCH;                // first output row
+        const int64_t r1 = r0 + P.RCH < P.p0_end ? r0 + P.RCH : P.p0_end;
+        const int64_t in_end = r1 + n0 - 1;                         // input rows [r0, in_end)
+        const int nbatch = (int)((in_end - r0 + NB - 1) / NB);
+        const bool col_ok = pbase + pos < P.P1;
+        C *obase = reinterpret_cast<C *>(P.out) + (pbase + pos) * (int64_t)(n0 * n1) + k1;
+
+        for (int b = 0; b < nbatch; ++b) {
+            const int64_t brow = r0 + (int64_t)b * NB;
+            // ---------------- stage R: row transforms of NB rows into the ring
+#pragma unroll
+            for (int tt = 0; tt < S::TPW; ++tt) {
+                const int task = warp + tt * S::WARPS;
+                if ((S::TASKS % S::WARPS) == 0 || task < S::TASKS) {
+                    const int rr = task / TPR, pg = task - rr * TPR;
+                    const int64_t row = brow + rr;
+                    const int pl = pg * GW + gam;
+                    const int64_t pcol = pbase + pl;
+                    C s[V];
+#pragma unroll
+                    for (int a = 0; a < V; ++a) {
+                        const int64_t col = pcol + lam + G * a;
+                        s[a] = (row < in_end && col < P.N1)
+                                   ? load_x<T>(P.x, P.in_dtype, row * P.ldx + col)
+                                   : mk<T>(0, 0);
+                    }
+                    // in-register levels (n1 > 32): classes c = lam + G*a
+#pragma unroll
+                    for (int L = 2; L <= V; L *= 2) {
+                        C ns[V];
+#pragma unroll
+                        for (int a = 0; a < V / L; ++a)
+#pragma unroll
+                            for (int i = 0; i < L; ++i) {
+                                const int ip = i % (L / 2);
+                                ns[a * L + i] = bfly<EXACT>(s[a * (L / 2) + ip],
+                                                            tw[i * (n1 / L) * ST1],
+                                                            s[(a + V / L) * (L / 2) + ip]);
+                            }
+#pragma unroll
+                        for (int a = 0; a < V; ++a) s[a] = ns[a];
+                    }
+                    // cross-lane levels: node (c, i) of slot be sits on lane (i/V)*(n1/L) + c
+#pragma unroll
+                    for (int L = 2 * V; L <= n1; L *= 2) {
+                        const int sL = n1 / L;
+                        const int c = lam % sL;
+#pragma unroll
+                        for (int be = 0; be < V; ++be) {
+                            const int i = (lam / sL) * V + be;
+                            const int ip = i % (L / 2);
+                            const int srcE = gam * G + (ip / V) * (2 * sL) + c;
+                            const int srcO = srcE + sL;
+                            C E, O;
+                            E.x = __shfl_sync(0xffffffffu, s[be].x, srcE);
+                            E.y = __shfl_sync(0xffffffffu, s[be].y, srcE);
+                            O.x = __shfl_sync(0xffffffffu, s[be].x, srcO);
+                            O.y = __shfl_sync(0xffffffffu, s[be].y, srcO);
+                            s[be] = bfly<EXACT>(E, tw[i * sL * ST1], O);
+                        }
+                    }
+                    if (pl < TP1) {
+                        C *dst = ring + ((b * NB + rr) & (D - 1)) * (TP1 * n1) + pl * n1 + lam * V;
+#pragma unroll
+                        for (int be = 0; be < V; ++be) dst[be] = s[be];
+                    }
+                }
+            }
+            __syncthreads();
+            // ---------------- stage C: column trees, NB rows
+#pragma unroll
+            for (int kk = 0; kk < NB; ++kk) {
+                const int rel = b * NB + kk;
+                C v[J];
+#pragma unroll
+                for (int t = 0; t < J; ++t)
+                    v[t] = ring[((rel - t * (n0 / J)) & (D - 1)) * (TP1 * n1) + pos * n1 + k1];
+                // levels 1..Q: node j of this row's tree (the reference DAG, tree2d.py:109-112)
+#pragma unroll
+                for (int l = 1; l <= Q; ++l) {
+                    const int sl = n0 >> l;
+                    const C w = tw[((j & ((1 << l) - 1)) * sl) * ST0];
+#pragma unroll
+                    for (int t = 0; t < (1 << (Q - l)); ++t)
+                        v[t] = bfly<EXACT>(v[t + (1 << (Q - l))], w, v[t]);
+                }
+                cur[0] = v[0];
+                // levels Q+1..m0 with reuse of the tree s_l rows back (register ring)
+#pragma unroll
+                for (int l = Q + 1; l <= M0; ++l) {
+                    const int sl = n0 >> l, h = 1 << (l - 1 - Q);
+                    const int off = (l - Q - 1) * (n0 / (2 * J)) + (kk % sl) * h;
+#pragma unroll
+                    for (int u = 0; u < h; ++u) {
+                        const C E = rring[off + u];
+                        const C O = cur[u];
+                        const int i = j + J * u;
+                        const C w0 = tw[(i * sl) * ST0];
+                        if constexpr (EXACT) {
+                            const C w1 = tw[((i + (1 << (l - 1))) * sl) * ST0];
+                            cur[u] = bfly_exact(E, w0, O);
+                            cur[u + h] = bfly_exact(E, w1, O);
+                        } else {
+                            const C t = cmul(w0, O);
+                            cur[u] = cadd(E, t);
+                            cur[u + h] = csub(E, t);
+                        }
+                        rring[off + u] = O;
+                    }
+                }
+                // emit window row p0 = r - (n0 - 1)
+                const int64_t p0 = r0 + rel - (n0 - 1);
+                if (rel >= n0 - 1 && p0 < r1 && col_ok) {
+                    C *o = obase + (p0 - P.p0_begin) * P.P1 * (int64_t)(n0 * n1);
+#pragma unroll
+                    for (int u = 0; u < S::OUTS; ++u) {
+                        C val = cur[u];
+                        if (P.apply_scale) val = cscale(val, (T)P.scale);
+                        st_stream(o + (j + J * u) * n1, val);
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// Per-instantiation launcher + registry entry.
+template <typename T, int M0, int M1, int Q, int TP1, bool EXACT>
+int k1_launch(const K1Params &P, int grid, cudaStream_t stream) {
+    using S = K1Shape<M0, M1, Q, TP1>;
+    constexpr size_t smem = k1_smem_bytes<T, M0, M1, Q, TP1>();
+    k1_stream_kernel<T, M0, M1, Q, TP1, EXACT><<<grid, S::NT, smem, stream>>>(P);
+    return 0;
+}
+
+// Heuristic shape per (m0, m1, precision): smallest J = 2^Q that keeps the
+// per-thread register ring <= RMAX complex and the per-row output count <= 16.
+constexpr int k1_choose_q(int M0, bool dbl) {
+    const int rmax = dbl ? 8 : 16, omax = dbl ? 8 : 16;
+    for (int q = 0; q <= M0; ++q) {
+        const int n0 = 1 << M0, J = 1 << q;
+        if ((M0 - q) * (n0 / (2 * J)) <= rmax && n0 / J <= omax) return q;
+    }
+    return M0;
+}
+constexpr int k1_choose_tp1(int M1, int Q) {
+    const int per = (1 << M1) * (1 << Q);
+    return per >= 256 ? 1 : 256 / per;
+}
+
+template <int M0, int M1, bool DBL> struct K1Inst {
+    using T = typename std::conditional<DBL, double, float>::type;
+    static constexpr int Q = k1_choose_q(M0, DBL);
+    static constexpr int TP1 = k1_choose_tp1(M1, Q);
+    using S = K1Shape<M0, M1, Q, TP1>;
+    static void reg() {
+        static const K1Info info = {
+            M0, M1, DBL ? 1 : 0, Q, TP1, S::NT, k1_smem_bytes<T, M0, M1, Q, TP1>(),
+            (const void *)&k1_stream_kernel<T, M0, M1, Q, TP1, DBL>,
+            &k1_launch<T, M0, M1, Q, TP1, DBL>};
+        register_k1(&info);
+    }
+};
+
+}  // namespace swdft2d

@@ -1,0 +1,107 @@
+// swdft2d_device.cuh — device-side building blocks shared by the K0 and K1 kernels.
+//
+// The one arithmetic primitive of the reference is core.butterfly
+// (/root/reference/pkg/src/swdft/core.py:223-246):
+//     out = shifted + twiddle * current
+//     re = fl(fl(wr*cr) - fl(wi*ci)),  im = fl(fl(wr*ci) + fl(wi*cr)),
+//     out = (fl(sr + re), fl(si + im))
+// Exact mode reproduces that rounding sequence with _rn intrinsics (no FMA
+// contraction), which is what makes the fp64 path bitwise equal to the
+// reference.  Fast (fp32) mode lets the compiler fuse into FFMAs.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace swdft2d {
+
+template <typename T> struct cplx_t;
+template <> struct cplx_t<float> { using type = float2; };
+template <> struct cplx_t<double> { using type = double2; };
+template <typename T> using cplx = typename cplx_t<T>::type;
+
+template <typename T> __device__ __forceinline__ cplx<T> mk(T re, T im) {
+    cplx<T> c;
+    c.x = re;
+    c.y = im;
+    return c;
+}
+
+// core.butterfly, bitwise (double) — shifted + w * current.
+__device__ __forceinline__ double2 bfly_exact(double2 s, double2 w, double2 c) {
+    double re = __dsub_rn(__dmul_rn(w.x, c.x), __dmul_rn(w.y, c.y));
+    double im = __dadd_rn(__dmul_rn(w.x, c.y), __dmul_rn(w.y, c.x));
+    return make_double2(__dadd_rn(s.x, re), __dadd_rn(s.y, im));
+}
+// core.butterfly with the same operation order in fp32 (used when EXACT on float,
+// i.e. never in product builds; kept for completeness of the template).
+__device__ __forceinline__ float2 bfly_exact(float2 s, float2 w, float2 c) {
+    float re = __fsub_rn(__fmul_rn(w.x, c.x), __fmul_rn(w.y, c.y));
+    float im = __fadd_rn(__fmul_rn(w.x, c.y), __fmul_rn(w.y, c.x));
+    return make_float2(__fadd_rn(s.x, re), __fadd_rn(s.y, im));
+}
+
+// Fast butterfly: s + w*c with FMAs.
+__device__ __forceinline__ float2 bfly_fast(float2 s, float2 w, float2 c) {
+    float re = fmaf(w.x, c.x, s.x);
+    re = fmaf(-w.y, c.y, re);
+    float im = fmaf(w.x, c.y, s.y);
+    im = fmaf(w.y, c.x, im);
+    return make_float2(re, im);
+}
+__device__ __forceinline__ double2 bfly_fast(double2 s, double2 w, double2 c) {
+    double re = fma(w.x, c.x, s.x);
+    re = fma(-w.y, c.y, re);
+    double im = fma(w.x, c.y, s.y);
+    im = fma(w.y, c.x, im);
+    return make_double2(re, im);
+}
+
+template <bool EXACT, typename C> __device__ __forceinline__ C bfly(C s, C w, C c) {
+    if constexpr (EXACT) return bfly_exact(s, w, c);
+    else return bfly_fast(s, w, c);
+}
+
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+    return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+
+// Per-component scaling, core.normalize (core.py:301): values * float64(factor).
+// Multiplying each component separately is bitwise equal to numpy's complex *
+// real-scalar product.
+__device__ __forceinline__ float2 cscale(float2 a, float f) { return make_float2(a.x * f, a.y * f); }
+__device__ __forceinline__ double2 cscale(double2 a, double f) {
+    return make_double2(__dmul_rn(a.x, f), __dmul_rn(a.y, f));
+}
+
+// Load element (row, col) of x with the given element type as complex<T>.
+// Real inputs get a +0.0 imaginary part, as np.asarray(x, complex128) does
+// (tree2d.py:189).  in_dtype is warp-uniform, so the switch does not diverge.
+template <typename T>
+__device__ __forceinline__ cplx<T> load_x(const void *__restrict__ x, int in_dtype, int64_t off) {
+    switch (in_dtype) {
+    case 0: return mk<T>((T)__ldg((const float *)x + off), (T)0);
+    case 1: return mk<T>((T)__ldg((const double *)x + off), (T)0);
+    case 2: {
+        float2 v = __ldg((const float2 *)x + off);
+        return mk<T>((T)v.x, (T)v.y);
+    }
+    default: {
+        double2 v = __ldg((const double2 *)x + off);
+        return mk<T>((T)v.x, (T)v.y);
+    }
+    }
+}
+
+// Streaming (evict-first) 8/16-byte stores for the write-once coefficient output.
+__device__ __forceinline__ void st_stream(float2 *p, float2 v) { __stcs(p, v); }
+__device__ __forceinline__ void st_stream(double2 *p, double2 v) { __stcs(p, v); }
+
+}  // namespace swdft2d

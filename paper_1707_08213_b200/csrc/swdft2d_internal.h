@@ -1,0 +1,50 @@
+// swdft2d_internal.h — host/device shared parameter blocks and launcher
+// prototypes (internal to libswdft2d.so; the public surface is include/swdft2d.h).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace swdft2d {
+
+constexpr int K1_TW_N = 64;    // K1 twiddle table: make_twiddles(64), read at stride 64/n
+constexpr int K0_TW_N = 1024;  // K0 twiddle table: make_twiddles(1024), in device memory
+
+struct K0Params {
+    const void *x;
+    int in_dtype, m0, m1, apply_scale;
+    int64_t ldx, p0_begin, p0_end, P1;
+    void *out;
+    double scale;
+    const void *tw;  // device table of K0_TW_N complex (float2 or double2)
+    int tw_n;
+};
+
+struct K1Params {
+    const void *x;
+    int in_dtype, apply_scale;
+    int64_t N0, N1, ldx;
+    int64_t p0_begin, p0_end, P1;
+    void *out;
+    double scale;
+    int64_t CB;      // column blocks of TP1 window positions
+    int64_t RCH;     // window rows per tile
+    int64_t ntiles;  // CB * ceil(rows / RCH)
+    double2 tw[K1_TW_N];
+};
+
+// Static shape of one K1 instantiation (filled by the instantiation units).
+struct K1Info {
+    int m0, m1, prec, q, tp1, threads;
+    size_t smem_bytes;
+    const void *func;  // kernel symbol for occupancy queries / attribute setting
+    int (*launch)(const K1Params &, int grid, cudaStream_t);
+};
+
+// Registry of compiled K1 instantiations; nullptr if (m0, m1, prec) is absent.
+const K1Info *find_k1(int m0, int m1, int prec);
+void register_k1(const K1Info *info);
+
+int launch_k0(const K0Params &P, int prec, cudaStream_t stream);
+
+}  // namespace swdft2d

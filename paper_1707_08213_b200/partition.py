@@ -1,0 +1,119 @@
+"""Single-box window-row strip partitioner (one process per GPU, torch.distributed).
+
+The batch 2D tree SWDFT shards exactly along window rows: window row p0 needs
+only input rows [p0, p0 + n0) and a strip of rows computed alone is bitwise
+identical to the same rows of a full run.  So the
+only data movement is a scatter of input strips (each with its n0 - 1 halo
+rows) from the rank that holds x; outputs stay resident on every rank and are
+never gathered or reduced.
+
+The reference has no multi-device path (its parallelism is a thread pool over
+contiguous axis-0 chunks per level, tree2d.py:22-27,58-64); the split rule here
+is the same "contiguous chunks of axis 0" idea applied once, across GPUs:
+rank g of G owns window rows [floor(P0*g/G), floor(P0*(g+1)/G))
+(swdft2d_strip_range in libswdft2d.so).
+
+The scatter is one batched group of point-to-point sends from ``src`` over the
+process group's backend (NCCL over NVLink/NVSwitch on the GPU box, gloo in the
+CPU tests).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+from . import _lib, core
+
+
+def strip_plan(P0: int, m0: int, world: int):
+    """[(p0_begin, p0_end, row_begin, row_end)] for every rank (via the C ABI)."""
+    return [_lib.strip_range(P0, m0, g, world) for g in range(world)]
+
+
+def strip_plan_py(P0: int, m0: int, world: int):
+    """Pure-Python statement of the same rule (used to cross-check the C ABI)."""
+    n0 = 1 << m0
+    out = []
+    for g in range(world):
+        a, b = (P0 * g) // world, (P0 * (g + 1)) // world
+        out.append((a, b, a, b + n0 - 1 if b > a else a))
+    return out
+
+
+@dataclass
+class ShardedCoefficients:
+    """This rank's window rows of the [P0, P1, n0, n1] output (device resident)."""
+
+    values: torch.Tensor
+    p0_begin: int
+    p0_end: int
+    source_shape: tuple
+    window: object
+    normalization: str = "none"
+
+
+def scatter_strips(x, shape, m0: int, dtype, device, group=None, src: int = 0):
+    """Scatter input row strips (with halos) from ``src``.
+
+    ``x`` (a tensor on ``device``, rows contiguous) is only read on ``src``; the
+    other ranks pass None.  Returns (local_rows_tensor, (p0_begin, p0_end,
+    row_begin, row_end)).  Empty strips (P0 < world) come back as 0-row tensors.
+    """
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    N0, N1 = int(shape[0]), int(shape[1])
+    P0 = N0 - (1 << m0) + 1
+    plan = strip_plan(P0, m0, world)
+    my = plan[rank]
+    ops = []
+    if rank == src:
+        if x is None or tuple(x.shape) != (N0, N1):
+            raise core.ShapeError(f"source rank needs the full {N0}x{N1} input")
+        for g, (_, _, rb, re) in enumerate(plan):
+            if g != src and re > rb:
+                ops.append(dist.P2POp(dist.isend, x[rb:re].contiguous(), g, group))
+        local = x[my[2]:my[3]]
+    else:
+        local = torch.empty((my[3] - my[2], N1), dtype=dtype, device=device)
+        if my[3] > my[2]:
+            ops.append(dist.P2POp(dist.irecv, local, src, group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    return local, my
+
+
+def tree_swdft_2d_sharded(x, spec, *, shape=None, dtype=None, group=None, src: int = 0,
+                          precision=None, budget=None) -> ShardedCoefficients:
+    """Strip-sharded tree_swdft_2d: every rank returns its own window rows.
+
+    On ``src`` pass the full input tensor (CUDA); elsewhere pass x=None plus
+    ``shape`` and ``dtype``.  Budget accounting is the reference's, per strip.
+    """
+    from .tree2d import _OUT_DTYPES, _precision_code, forward_into
+
+    rank = dist.get_rank(group)
+    if rank == src:
+        shape = tuple(int(s) for s in x.shape)
+        dtype = x.dtype
+        device = x.device
+    else:
+        device = torch.device("cuda", torch.cuda.current_device())
+    if len(shape) != 2 or len(spec.exponents) != 2:
+        raise core.ShapeError("tree_swdft_2d expects a 2D array and 2D window")
+    spec.check_fits(shape)
+    m0, m1 = (int(m) for m in spec.exponents)
+    local, (a, b, rb, re) = scatter_strips(x, shape, m0, dtype, device, group, src)
+    prec = _precision_code(precision, dtype)
+    n0, n1 = 1 << m0, 1 << m1
+    P1 = shape[1] - n1 + 1
+    if b > a:
+        sshape = (re - rb, shape[1])
+        core.check_budget(core.lattice_bytes(sshape, spec) + core.output_bytes(sshape, spec),
+                          budget, what="level buffers + coefficient output")
+    out = torch.empty((b - a, P1, n0, n1), dtype=_OUT_DTYPES[prec], device=device)
+    if b > a:
+        forward_into(local, m0, m1, out, prec=prec, scale=core.normalization_factor(spec))
+    return ShardedCoefficients(out, a, b, tuple(shape), spec, spec.normalization)

@@ -1,0 +1,240 @@
+"""GPU parity: libswdft2d.so (through the C ABI / drop-in wrapper) vs the pinned oracle
+and the reference's golden vectors.
+
+fp64 ("DAG-exact") must be BITWISE equal to the reference.  fp32 must satisfy
+BASELINE.json's tolerance: max_k |a_gpu - a_ref| / ||a_ref window||_2 <= 1e-4.
+"""
+import numpy as np
+import pytest
+import torch
+
+from conftest import sha
+from golden_inputs import acc_input, kat6_input
+from paper_1707_08213_b200 import (BudgetError, OpCounter, ShapeError, WindowSpec,
+                                   WindowTooLargeError, forward_into, tree_swdft_2d)
+from paper_1707_08213_b200 import _lib
+from paper_1707_08213_b200.workloads import CONFIGS
+
+pytestmark = pytest.mark.gpu
+
+FP32_TOL = 1e-4  # BASELINE.json north_star, complex64 mode
+FP64_TOL = 1e-10  # BASELINE.json north_star, fp64 mode (we require bitwise anyway)
+KERNELS = ("stream", "window")
+
+
+def rel_err(got, ref):
+    import oracle
+
+    return oracle.window_rel_err(got, ref)
+
+
+def run(x, m0, m1, precision, kernel="auto", normalization="none"):
+    spec = WindowSpec((m0, m1), normalization)
+    res = tree_swdft_2d(x, spec, precision=precision, kernel=kernel, budget=1 << 62)
+    return res.values.cpu().numpy()
+
+
+def bits_equal(a, b):
+    return a.shape == b.shape and np.array_equal(a.view(np.uint64), b.view(np.uint64))
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_kats_fp64_bitwise(golden, cuda, kernel):
+    meta, arr = golden
+    x = np.array(meta["kat"]["kat1"]["x"])
+    assert bits_equal(run(x, 1, 1, "fp64", kernel), arr["kat1_out"])
+    assert bits_equal(run(np.ones((8, 8)), 2, 2, "fp64", kernel), arr["kat2_out"])
+    k6, nx = kat6_input()
+    assert bits_equal(run(k6, 1, 2, "fp64", kernel), arr["kat6_out"])
+    for mode in ("unitary", "paper-2d"):
+        assert bits_equal(run(nx, 2, 1, "fp64", kernel, mode), arr[f"norm_{mode}_out"])
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_acceptance_sweep_fp64_bitwise(golden, cuda, kernel):
+    """SPEC.md acceptance 1+2 on the GPU: 800 (array, window) cases, SHA-256 equal to the reference."""
+    meta, _ = golden
+    bad = []
+    for rec in meta["acc"]:
+        x = acc_input(rec["case"])
+        out = run(x, rec["m0"], rec["m1"], "fp64", kernel)
+        if sha(out) != rec["sha"]:
+            bad.append((rec["case"], rec["m0"], rec["m1"]))
+    assert not bad, f"{len(bad)} mismatches, first {bad[:5]}"
+
+
+def test_acceptance_sweep_fp32_tolerance(cuda, oracle_lib):
+    for case in range(0, 50, 3):
+        x = acc_input(case)
+        for m0 in range(4):
+            for m1 in range(4):
+                if (1 << m0) > x.shape[0] or (1 << m1) > x.shape[1]:
+                    continue
+                ref = oracle_lib.tree2d(x, m0, m1)
+                for kernel in KERNELS:
+                    got = run(x.astype(np.complex64), m0, m1, "fp32", kernel)
+                    assert rel_err(got, ref) <= FP32_TOL
+
+
+@pytest.mark.parametrize("kernel", KERNELS)
+def test_config1_full_bitwise(golden, cuda, kernel):
+    meta, _ = golden
+    cfg = CONFIGS["c1"]
+    x = cfg.generate()
+    out = run(x, cfg.m0, cfg.m1, "fp64", kernel)
+    assert sha(out) == meta["configs"]["c1"]["full_sha"]
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
+def test_config_strips_fp64_bitwise_and_fp32(golden, cuda, oracle_lib, name):
+    """Small strips of configs 2-5: fp64 mode bitwise vs the reference's SHA-256;
+    fp32 mode within tolerance of the (pinned) oracle."""
+    meta, _ = golden
+    cfg = CONFIGS[name]
+    x = cfg.generate()
+    assert sha(x) == meta["configs"][name]["in_sha"]
+    for st in meta["configs"][name]["strips"]:
+        sub = x[st["p0"]:st["p0"] + st["rows"] + cfg.n0 - 1, st["p1"]:st["p1"] + st["cols"] + cfg.n1 - 1]
+        sub = np.ascontiguousarray(sub)
+        for kernel in KERNELS:
+            assert sha(run(sub, cfg.m0, cfg.m1, "fp64", kernel)) == st["sha"]
+        ref = oracle_lib.tree2d(sub, cfg.m0, cfg.m1)
+        for kernel in KERNELS:
+            assert rel_err(run(sub, cfg.m0, cfg.m1, "fp32", kernel), ref) <= FP32_TOL
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c4", "c5"])
+def test_config_full_size_fp32(golden, cuda, name):
+    """The full BASELINE config on the GPU (complex64): sampled windows vs the
+    reference's golden values and numpy fft2; size-independent properties over
+    EVERY window: DC = window sum and Parseval, against fp64 box sums."""
+    meta, arr = golden
+    cfg = CONFIGS[name]
+    x = cfg.generate()
+    spec = WindowSpec((cfg.m0, cfg.m1))
+    res = tree_swdft_2d(x, spec, budget=1 << 62)
+    vals = res.values
+    assert vals.dtype == torch.complex64 and tuple(vals.shape) == (cfg.P0, cfg.P1, cfg.n0, cfg.n1)
+    for (p0, p1), ref in zip(arr[f"{name}_win_pos"], arr[f"{name}_win_out"]):
+        got = vals[p0, p1].cpu().numpy()[None, None]
+        assert rel_err(got, ref[None, None]) <= FP32_TOL
+        f = np.fft.fft2(x[p0:p0 + cfg.n0, p1:p1 + cfg.n1].astype(np.complex128))
+        assert rel_err(got, f[None, None]) <= FP32_TOL
+    # every window: DC coefficient and Parseval, via fp64 summed-area tables on device
+    xd = torch.from_numpy(np.ascontiguousarray(x)).to(cuda).to(torch.complex128)
+    n0, n1 = cfg.n0, cfg.n1
+
+    def box(t):
+        s = torch.zeros((t.shape[0] + 1, t.shape[1] + 1), dtype=t.dtype, device=t.device)
+        s[1:, 1:] = t.cumsum(0).cumsum(1)
+        return s[n0:, n1:] - s[:-n0, n1:] - s[n0:, :-n1] + s[:-n0, :-n1]
+
+    dc_ref = box(xd)
+    en_ref = box(xd.abs() ** 2).real * (n0 * n1)
+    chunk = max(1, (1 << 28) // (cfg.P1 * n0 * n1))
+    worst_dc = worst_en = 0.0
+    for a in range(0, cfg.P0, chunk):
+        b = min(cfg.P0, a + chunk)
+        v = vals[a:b]
+        nrm = (v.abs().double() ** 2).sum((-1, -2))
+        win_norm = torch.sqrt(en_ref[a:b]).clamp_min(1e-30)
+        worst_dc = max(worst_dc, float(((v[..., 0, 0].to(torch.complex128) - dc_ref[a:b]).abs() / win_norm).max()))
+        worst_en = max(worst_en, float(((nrm - en_ref[a:b]).abs() / en_ref[a:b].clamp_min(1e-30)).max()))
+    assert worst_dc <= FP32_TOL, worst_dc
+    assert worst_en <= 2e-4, worst_en
+    del vals, res
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("shape,m", [
+    ((8, 8), (3, 3)),      # n = N: a single window position
+    ((9, 40), (0, 3)),     # n0 = 1
+    ((40, 9), (3, 0)),     # n1 = 1
+    ((5, 7), (0, 0)),      # 1x1 windows
+    ((37, 29), (2, 4)),    # odd extents, non-square
+    ((70, 130), (6, 6)),   # 64x64 windows (K1 V=2 path)
+    ((100, 70), (5, 1)),   # n1 < 32, deep dim 0
+    ((33, 300), (1, 6)),
+    ((300, 20), (6, 2)),
+])
+def test_edge_shapes(cuda, oracle_lib, shape, m):
+    rng = np.random.default_rng(sum(shape) + 7 * m[0] + m[1])
+    x = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    ref = oracle_lib.tree2d(x, *m)
+    for kernel in KERNELS:
+        assert bits_equal(run(x, *m, "fp64", kernel), ref), kernel
+        assert rel_err(run(x.astype(np.complex64), *m, "fp32", kernel), ref) <= FP32_TOL
+
+
+def test_input_dtypes_and_strides(cuda, oracle_lib):
+    rng = np.random.default_rng(5)
+    xr = rng.standard_normal((50, 45))
+    ref = oracle_lib.tree2d(xr, 3, 2)
+    assert bits_equal(run(xr, 3, 2, "fp64"), ref)                       # float64
+    assert bits_equal(run(xr.astype(np.complex128), 3, 2, "fp64"), ref)  # complex128
+    xi = rng.integers(-5, 5, (50, 45))
+    assert bits_equal(run(xi, 3, 2, "fp64"), oracle_lib.tree2d(xi.astype(float), 3, 2))
+    x32 = xr.astype(np.float32)
+    assert bits_equal(run(x32, 3, 2, "fp64"), oracle_lib.tree2d(x32.astype(np.float64), 3, 2))
+    assert rel_err(run(x32, 3, 2, None), ref) <= FP32_TOL                # default fp32 for f32
+    # a strided device view (row stride > width) goes through ld_x
+    big = torch.from_numpy(xr).to(cuda)
+    pad = torch.zeros((50, 64), dtype=torch.float64, device=cuda)
+    pad[:, :45] = big
+    view = pad[:, :45]
+    assert view.stride(0) == 64
+    out = torch.empty((47, 42, 8, 4), dtype=torch.complex128, device=cuda)
+    forward_into(view, 3, 2, out, prec=_lib.PREC_FP64)
+    assert bits_equal(out.cpu().numpy(), ref)
+
+
+def test_row_ranges(cuda, oracle_lib):
+    """swdft2d_forward on window-row sub-ranges (the strip boundary) is bitwise exact."""
+    rng = np.random.default_rng(9)
+    x = rng.standard_normal((90, 60))
+    ref = oracle_lib.tree2d(x, 4, 3)
+    xt = torch.from_numpy(x).to(cuda)
+    for (a, b) in [(0, 1), (5, 40), (74, 75), (30, 75)]:
+        for kernel in KERNELS:
+            out = torch.empty((b - a, 53, 16, 8), dtype=torch.complex128, device=cuda)
+            forward_into(xt, 4, 3, out, prec=_lib.PREC_FP64, p0_begin=a, p0_end=b, kernel=kernel)
+            assert bits_equal(out.cpu().numpy(), ref[a:b])
+
+
+def test_wrapper_contract(cuda, golden):
+    meta, _ = golden
+    x = np.random.default_rng(1).standard_normal((20, 17))
+    with pytest.raises(ShapeError):
+        tree_swdft_2d(x[0], WindowSpec((1, 1)))
+    with pytest.raises(WindowTooLargeError):
+        tree_swdft_2d(x, WindowSpec((5, 1)))
+    with pytest.raises(ValueError):
+        tree_swdft_2d(x, WindowSpec((1, 1)), loop_order="bogus")
+    with pytest.raises(BudgetError):
+        tree_swdft_2d(np.ones((8, 8)), WindowSpec((1, 1)), budget=10)
+    # OpCounter replay equals the reference's counts, both loop orders
+    for rec in meta["opcount"]:
+        xx = np.random.default_rng(rec["N0"] * 100 + rec["N1"]).standard_normal((rec["N0"], rec["N1"]))
+        for order in ("levels-outer", "trees-outer"):
+            c = OpCounter((rec["N0"], rec["N1"]))
+            r = tree_swdft_2d(xx, WindowSpec((rec["m0"], rec["m1"])), loop_order=order, counter=c)
+            assert c.total == rec[order]["total"]
+            assert sha(c.position_ops) == rec[order]["pos_sha"]
+            assert r.values.is_cuda
+    # both loop orders give identical output
+    a = tree_swdft_2d(x, WindowSpec((2, 2)), loop_order="levels-outer").values
+    b = tree_swdft_2d(x, WindowSpec((2, 2)), loop_order="trees-outer").values
+    assert torch.equal(a, b)
+
+
+def test_linearity_and_transpose(cuda):
+    """SPEC.md:350-351 properties on the device path (fp64)."""
+    rng = np.random.default_rng(2)
+    x = rng.standard_normal((24, 20)) + 1j * rng.standard_normal((24, 20))
+    y = rng.standard_normal((24, 20)) + 1j * rng.standard_normal((24, 20))
+    a, b = 0.7 - 0.2j, -1.3 + 0.5j
+    lhs = run(a * x + b * y, 3, 2, "fp64")
+    rhs = a * run(x, 3, 2, "fp64") + b * run(y, 3, 2, "fp64")
+    assert np.abs(lhs - rhs).max() <= 1e-10 * max(1, np.abs(rhs).max())
+    xt = run(np.ascontiguousarray(x.T), 2, 3, "fp64")
+    assert np.abs(xt - run(x, 3, 2, "fp64").transpose(1, 0, 3, 2)).max() <= 1e-10
