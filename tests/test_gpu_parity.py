@@ -183,7 +183,7 @@ def test_input_dtypes_and_strides(cuda, oracle_lib):
     pad[:, :45] = big
     view = pad[:, :45]
     assert view.stride(0) == 64
-    out = torch.empty((47, 42, 8, 4), dtype=torch.complex128, device=cuda)
+    out = torch.empty((43, 42, 8, 4), dtype=torch.complex128, device=cuda)
     forward_into(view, 3, 2, out, prec=_lib.PREC_FP64)
     assert bits_equal(out.cpu().numpy(), ref)
 
