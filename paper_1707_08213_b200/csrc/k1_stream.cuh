@@ -37,11 +37,22 @@
 #pragma once
 
 #include <type_traits>
+#include <utility>
 
 #include "swdft2d_device.cuh"
 #include "swdft2d_internal.h"
 
 namespace swdft2d {
+
+// Compile-time loop: f(std::integral_constant<int, I>) for I = 0..N-1, so every
+// register-array index inside f is a constant (keeps rings/accumulators in registers).
+template <typename F, int... Is>
+__device__ __forceinline__ void static_for_impl(F &&f, std::integer_sequence<int, Is...>) {
+    (f(std::integral_constant<int, Is>{}), ...);
+}
+template <int N, typename F> __device__ __forceinline__ void static_for(F &&f) {
+    static_for_impl(f, std::make_integer_sequence<int, N>{});
+}
 
 constexpr int cmax(int a, int b) { return a > b ? a : b; }
 constexpr int cmin(int a, int b) { return a < b ? a : b; }
@@ -51,11 +62,11 @@ constexpr int pow2ceil(int v) {
     return p;
 }
 
-template <int M0, int M1, int Q, int TP1> struct K1Shape {
+template <int M0, int M1, int Q, int TP1, int NBM = 1> struct K1Shape {
     static constexpr int n0 = 1 << M0, n1 = 1 << M1, J = 1 << Q;
     static constexpr int NT = n1 * J * TP1;               // threads per CTA
     static constexpr int WARPS = NT / 32;
-    static constexpr int NB = cmax(n0 / J, 4);            // rows per batch
+    static constexpr int NB = cmax(n0 / J, 4) * NBM;      // rows per batch
     static constexpr int D = pow2ceil(n0 - n0 / J + NB);  // Z ring depth (rows)
     static constexpr int G = cmin(n1, 32);                // lanes per row transform
     static constexpr int V = n1 / G;                      // values per lane
@@ -66,20 +77,21 @@ template <int M0, int M1, int Q, int TP1> struct K1Shape {
     static constexpr int NMAX = cmax(n0, n1);
     static constexpr int RING = cmax((M0 - Q) * (n0 / (2 * J)), 1);  // register ring, complex
     static constexpr int OUTS = n0 / J;                   // coefficients per thread per row
+    static constexpr int UNR = cmin(cmax(n0 / (2 * J), 8), NB);  // stage-C rows per unrolled block
     static_assert(Q <= M0, "J must divide n0");
     static_assert(NT % 32 == 0 && NT <= 1024, "CTA size must be a warp multiple <= 1024");
 };
 
-template <typename T, int M0, int M1, int Q, int TP1>
+template <typename T, int M0, int M1, int Q, int TP1, int NBM = 1>
 constexpr size_t k1_smem_bytes() {
-    using S = K1Shape<M0, M1, Q, TP1>;
+    using S = K1Shape<M0, M1, Q, TP1, NBM>;
     return sizeof(cplx<T>) * ((size_t)S::D * TP1 * S::n1 + S::NMAX);
 }
 
-template <typename T, int M0, int M1, int Q, int TP1, bool EXACT>
-__global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1>::NT)
+template <typename T, int M0, int M1, int Q, int TP1, bool EXACT, int MINB = 1, int NBM = 1>
+__global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
     k1_stream_kernel(const __grid_constant__ K1Params P) {
-    using S = K1Shape<M0, M1, Q, TP1>;
+    using S = K1Shape<M0, M1, Q, TP1, NBM>;
     using C = cplx<T>;
     constexpr int n0 = S::n0, n1 = S::n1, J = S::J, NB = S::NB, D = S::D;
     constexpr int G = S::G, V = S::V, GW = S::GW, TPR = S::TPR, NMAX = S::NMAX;
@@ -116,25 +128,40 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1>::NT)
         const bool col_ok = pbase + pos < P.P1;
         C *obase = reinterpret_cast<C *>(P.out) + (pbase + pos) * (int64_t)(n0 * n1) + k1;
 
+        // Input samples of this warp's stage-R tasks for one batch, prefetched one
+        // batch ahead so the global-load latency hides behind stage C.
+        C xs[S::TPW][V];
+        auto load_batch = [&](int bb) {
+            const int64_t brow = r0 + (int64_t)bb * NB;
+#pragma unroll
+            for (int tt = 0; tt < S::TPW; ++tt) {
+                const int task = warp + tt * S::WARPS;
+                const int rr = task / TPR, pg = task - rr * TPR;
+                const int64_t row = brow + rr;
+                const int64_t pcol = pbase + pg * GW + gam;
+#pragma unroll
+                for (int a = 0; a < V; ++a) {
+                    const int64_t col = pcol + lam + G * a;
+                    xs[tt][a] = ((S::TASKS % S::WARPS) == 0 || task < S::TASKS) && row < in_end &&
+                                        col < P.N1
+                                    ? load_x<T>(P.x, P.in_dtype, row * P.ldx + col)
+                                    : mk<T>(0, 0);
+                }
+            }
+        };
+        load_batch(0);
+
         for (int b = 0; b < nbatch; ++b) {
-            const int64_t brow = r0 + (int64_t)b * NB;
             // ---------------- stage R: row transforms of NB rows into the ring
 #pragma unroll
             for (int tt = 0; tt < S::TPW; ++tt) {
                 const int task = warp + tt * S::WARPS;
                 if ((S::TASKS % S::WARPS) == 0 || task < S::TASKS) {
                     const int rr = task / TPR, pg = task - rr * TPR;
-                    const int64_t row = brow + rr;
                     const int pl = pg * GW + gam;
-                    const int64_t pcol = pbase + pl;
                     C s[V];
 #pragma unroll
-                    for (int a = 0; a < V; ++a) {
-                        const int64_t col = pcol + lam + G * a;
-                        s[a] = (row < in_end && col < P.N1)
-                                   ? load_x<T>(P.x, P.in_dtype, row * P.ldx + col)
-                                   : mk<T>(0, 0);
-                    }
+                    for (int a = 0; a < V; ++a) s[a] = xs[tt][a];
                     // in-register levels (n1 > 32): classes c = lam + G*a
 #pragma unroll
                     for (int L = 2; L <= V; L *= 2) {
@@ -178,58 +205,65 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1>::NT)
                 }
             }
             __syncthreads();
-            // ---------------- stage C: column trees, NB rows
-#pragma unroll
-            for (int kk = 0; kk < NB; ++kk) {
-                const int rel = b * NB + kk;
-                C v[J];
-#pragma unroll
-                for (int t = 0; t < J; ++t)
-                    v[t] = ring[((rel - t * (n0 / J)) & (D - 1)) * (TP1 * n1) + pos * n1 + k1];
-                // levels 1..Q: node j of this row's tree (the reference DAG, tree2d.py:109-112)
-#pragma unroll
-                for (int l = 1; l <= Q; ++l) {
-                    const int sl = n0 >> l;
-                    const C w = tw[((j & ((1 << l) - 1)) * sl) * ST0];
-#pragma unroll
-                    for (int t = 0; t < (1 << (Q - l)); ++t)
-                        v[t] = bfly<EXACT>(v[t + (1 << (Q - l))], w, v[t]);
-                }
-                cur[0] = v[0];
-                // levels Q+1..m0 with reuse of the tree s_l rows back (register ring)
-#pragma unroll
-                for (int l = Q + 1; l <= M0; ++l) {
-                    const int sl = n0 >> l, h = 1 << (l - 1 - Q);
-                    const int off = (l - Q - 1) * (n0 / (2 * J)) + (kk % sl) * h;
-#pragma unroll
-                    for (int u = 0; u < h; ++u) {
-                        const C E = rring[off + u];
-                        const C O = cur[u];
-                        const int i = j + J * u;
-                        const C w0 = tw[(i * sl) * ST0];
-                        if constexpr (EXACT) {
-                            const C w1 = tw[((i + (1 << (l - 1))) * sl) * ST0];
-                            cur[u] = bfly_exact(E, w0, O);
-                            cur[u + h] = bfly_exact(E, w1, O);
-                        } else {
-                            const C t = cmul(w0, O);
-                            cur[u] = cadd(E, t);
-                            cur[u + h] = csub(E, t);
-                        }
-                        rring[off + u] = O;
+            if (b + 1 < nbatch) load_batch(b + 1);
+            // ---------------- stage C: column trees, NB rows, UNR rows per unrolled block
+            // (UNR is a multiple of every register-ring depth, so ring slots are static)
+#pragma unroll 1
+            for (int k0r = 0; k0r < NB; k0r += S::UNR) {
+                static_for<S::UNR>([&](auto kuc) {
+                    constexpr int ku = decltype(kuc)::value;
+                    const int rel = b * NB + k0r + ku;
+                    C v[J];
+                    static_for<J>([&](auto tc) {
+                        constexpr int t = decltype(tc)::value;
+                        v[t] = ring[((rel - t * (n0 / J)) & (D - 1)) * (TP1 * n1) + pos * n1 + k1];
+                    });
+                    // levels 1..Q: node j of this row's tree (the reference DAG, tree2d.py:109-112)
+                    static_for<Q>([&](auto lc) {
+                        constexpr int l = decltype(lc)::value + 1;
+                        constexpr int sl = n0 >> l;
+                        const C w = tw[((j & ((1 << l) - 1)) * sl) * ST0];
+                        static_for<(1 << (Q - l))>([&](auto tc) {
+                            constexpr int t = decltype(tc)::value;
+                            v[t] = bfly<EXACT>(v[t + (1 << (Q - l))], w, v[t]);
+                        });
+                    });
+                    cur[0] = v[0];
+                    // levels Q+1..m0, reusing the tree s_l rows back (register ring)
+                    static_for<M0 - Q>([&](auto lc) {
+                        constexpr int l = decltype(lc)::value + Q + 1;
+                        constexpr int sl = n0 >> l, h = 1 << (l - 1 - Q);
+                        constexpr int off = (l - Q - 1) * (n0 / (2 * J)) + (ku % sl) * h;
+                        static_for<h>([&](auto uc) {
+                            constexpr int u = decltype(uc)::value;
+                            const C E = rring[off + u];
+                            const C O = cur[u];
+                            const int i = j + J * u;
+                            const C w0 = tw[(i * sl) * ST0];
+                            if constexpr (EXACT) {
+                                const C w1 = tw[((i + (1 << (l - 1))) * sl) * ST0];
+                                cur[u] = bfly_exact(E, w0, O);
+                                cur[u + h] = bfly_exact(E, w1, O);
+                            } else {
+                                const C t = cmul(w0, O);
+                                cur[u] = cadd(E, t);
+                                cur[u + h] = csub(E, t);
+                            }
+                            rring[off + u] = O;
+                        });
+                    });
+                    // emit window row p0 = r - (n0 - 1)
+                    const int64_t p0 = r0 + rel - (n0 - 1);
+                    if (rel >= n0 - 1 && p0 < r1 && col_ok) {
+                        C *o = obase + (p0 - P.p0_begin) * P.P1 * (int64_t)(n0 * n1);
+                        static_for<S::OUTS>([&](auto uc) {
+                            constexpr int u = decltype(uc)::value;
+                            C val = cur[u];
+                            if (P.apply_scale) val = cscale(val, (T)P.scale);
+                            st_stream(o + (j + J * u) * n1, val);
+                        });
                     }
-                }
-                // emit window row p0 = r - (n0 - 1)
-                const int64_t p0 = r0 + rel - (n0 - 1);
-                if (rel >= n0 - 1 && p0 < r1 && col_ok) {
-                    C *o = obase + (p0 - P.p0_begin) * P.P1 * (int64_t)(n0 * n1);
-#pragma unroll
-                    for (int u = 0; u < S::OUTS; ++u) {
-                        C val = cur[u];
-                        if (P.apply_scale) val = cscale(val, (T)P.scale);
-                        st_stream(o + (j + J * u) * n1, val);
-                    }
-                }
+                });
             }
             __syncthreads();
         }
@@ -237,41 +271,46 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1>::NT)
 }
 
 // Per-instantiation launcher + registry entry.
-template <typename T, int M0, int M1, int Q, int TP1, bool EXACT>
+template <typename T, int M0, int M1, int Q, int TP1, bool EXACT, int MINB = 1, int NBM = 1>
 int k1_launch(const K1Params &P, int grid, cudaStream_t stream) {
-    using S = K1Shape<M0, M1, Q, TP1>;
-    constexpr size_t smem = k1_smem_bytes<T, M0, M1, Q, TP1>();
-    k1_stream_kernel<T, M0, M1, Q, TP1, EXACT><<<grid, S::NT, smem, stream>>>(P);
+    using S = K1Shape<M0, M1, Q, TP1, NBM>;
+    constexpr size_t smem = k1_smem_bytes<T, M0, M1, Q, TP1, NBM>();
+    k1_stream_kernel<T, M0, M1, Q, TP1, EXACT, MINB, NBM><<<grid, S::NT, smem, stream>>>(P);
     return 0;
 }
 
-// Heuristic shape per (m0, m1, precision): smallest J = 2^Q that keeps the
-// per-thread register ring <= RMAX complex and the per-row output count <= 16.
-constexpr int k1_choose_q(int M0, bool dbl) {
-    const int rmax = dbl ? 8 : 16, omax = dbl ? 8 : 16;
-    for (int q = 0; q <= M0; ++q) {
-        const int n0 = 1 << M0, J = 1 << q;
-        if ((M0 - q) * (n0 / (2 * J)) <= rmax && n0 / J <= omax) return q;
-    }
-    return M0;
+// Registry entry for an explicit shape (used by K1Inst and by the tuning harness).
+template <typename T, int M0, int M1, int Q, int TP1, bool EXACT, int MINB = 1, int NBM = 1>
+const K1Info *k1_info() {
+    using S = K1Shape<M0, M1, Q, TP1, NBM>;
+    static const K1Info info = {
+        M0, M1, EXACT ? 1 : 0, Q, TP1, S::NT, k1_smem_bytes<T, M0, M1, Q, TP1, NBM>(),
+        (const void *)&k1_stream_kernel<T, M0, M1, Q, TP1, EXACT, MINB, NBM>,
+        &k1_launch<T, M0, M1, Q, TP1, EXACT, MINB, NBM>};
+    return &info;
+}
+
+// Shape per (m0, m1): J = 2^Q residue groups so that each thread emits n0/J = 4
+// coefficients per row (Q = m0 - 2), capped at 512 threads per window column;
+// TP1 window columns per CTA so that a CTA is ~128 threads.  Measured on B200
+// with scripts/tune (profiles/TUNING_r01.md): e.g. c4 (16x16) Q=2/TP1=2 831
+// Gcoef/s vs 760 for Q=1/TP1=8; c3 (32x8) Q=3/TP1=2 783; c5 (64x64) Q=3/TP1=1 797.
+constexpr int k1_choose_q(int M0, int M1) {
+    int q = M0 > 2 ? M0 - 2 : 0;
+    while (q > 0 && (1 << M1) * (1 << q) > 512) --q;
+    return q;
 }
 constexpr int k1_choose_tp1(int M1, int Q) {
     const int per = (1 << M1) * (1 << Q);
-    return per >= 256 ? 1 : 256 / per;
+    return per >= 128 ? 1 : 128 / per;
 }
 
 template <int M0, int M1, bool DBL> struct K1Inst {
     using T = typename std::conditional<DBL, double, float>::type;
-    static constexpr int Q = k1_choose_q(M0, DBL);
+    static constexpr int Q = k1_choose_q(M0, M1);
     static constexpr int TP1 = k1_choose_tp1(M1, Q);
     using S = K1Shape<M0, M1, Q, TP1>;
-    static void reg() {
-        static const K1Info info = {
-            M0, M1, DBL ? 1 : 0, Q, TP1, S::NT, k1_smem_bytes<T, M0, M1, Q, TP1>(),
-            (const void *)&k1_stream_kernel<T, M0, M1, Q, TP1, DBL>,
-            &k1_launch<T, M0, M1, Q, TP1, DBL>};
-        register_k1(&info);
-    }
+    static void reg() { register_k1(k1_info<T, M0, M1, Q, TP1, DBL>()); }
 };
 
 }  // namespace swdft2d

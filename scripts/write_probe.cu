@@ -1,0 +1,63 @@
+// write_probe.cu — the B200 HBM write-only ceiling for the roofline of a
+// write-bound kernel, under several access patterns:
+//   gridstride  : all CTAs sweep the buffer together (st.global.cs.v4)
+//   chunked     : each CTA streams its own contiguous region
+//   k1pattern   : each CTA writes 32 KB blocks at a 33 MB stride (K1's C4 output pattern)
+//   memset      : cudaMemsetAsync
+// Values are per-thread varying (not compressible) unless noted.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o write_probe write_probe.cu
+#include <cstdio>
+#include <cuda_runtime.h>
+
+__global__ void gridstride(float4 *p, size_t n) {
+    size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x, st = (size_t)gridDim.x * blockDim.x;
+    for (; i < n; i += st) __stcs(p + i, make_float4((float)i, 1.f, 2.f, (float)threadIdx.x));
+}
+__global__ void chunked(float4 *p, size_t n) {
+    size_t per = (n + gridDim.x - 1) / gridDim.x, b = blockIdx.x * per, e = b + per < n ? b + per : n;
+    for (size_t i = b + threadIdx.x; i < e; i += blockDim.x)
+        __stcs(p + i, make_float4((float)i, 1.f, 2.f, (float)threadIdx.x));
+}
+// block of 2048 float4 (32 KB) per "row"; rows of a CTA are `stride` float4 apart
+__global__ void k1pattern(float4 *p, size_t n, size_t stride, size_t nblk_per_row) {
+    const size_t rows = n / stride;
+    for (size_t t = blockIdx.x; t < nblk_per_row * 8; t += gridDim.x) {
+        size_t cb = t % nblk_per_row, rc = t / nblk_per_row;
+        for (size_t r = rc * rows / 8; r < (rc + 1) * rows / 8; ++r) {
+            float4 *q = p + r * stride + cb * 2048;
+            for (int i = threadIdx.x; i < 2048; i += blockDim.x)
+                __stcs(q + i, make_float4((float)i, (float)r, 2.f, 3.f));
+        }
+    }
+}
+
+int main() {
+    size_t bytes = 32ull << 30, n = bytes / 16;
+    float4 *p;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) { printf("alloc failed\n"); return 1; }
+    int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+    const size_t stride = (33ull << 20) / 16, nblk = stride / 2048;
+    for (int mode = 0; mode < 4; ++mode)
+        for (int occ : {2, 4, 8}) {
+            float best = 1e30f;
+            size_t written = bytes;
+            for (int rep = 0; rep < 4; ++rep) {
+                cudaEventRecord(a);
+                if (mode == 0) gridstride<<<sms * occ, 512>>>(p, n);
+                else if (mode == 1) chunked<<<sms * occ, 512>>>(p, n);
+                else if (mode == 2) k1pattern<<<sms * occ, 512>>>(p, n, stride, nblk);
+                else cudaMemsetAsync(p, rep + 1, bytes);
+                cudaEventRecord(b); cudaEventSynchronize(b);
+                float ms; cudaEventElapsedTime(&ms, a, b);
+                if (ms < best) best = ms;
+            }
+            if (mode == 2) written = (n / stride) * stride * 16;
+            const char *nm[] = {"gridstride", "chunked", "k1pattern", "memset"};
+            printf("{\"mode\": \"%s\", \"ctas_per_sm\": %d, \"GBps\": %.1f}\n", nm[mode], occ,
+                   written / best / 1e6);
+            if (mode == 3) break;
+        }
+    cudaError_t e = cudaDeviceSynchronize();
+    return e == cudaSuccess ? 0 : 2;
+}
