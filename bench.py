@@ -248,8 +248,11 @@ def run_ours(args, cfg, rank, world, local_rank):
         # one step = one K1 launch; replaying it from a CUDA graph keeps host-side
         # launch overhead out of the device-timed region
         graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph, stream=stream):
-            forward_into(x_full, cfg.m0, cfg.m1, out, prec=prec, stream=stream)
+        cap = torch.cuda.Stream(dev)  # graphs are captured on a side stream
+        cap.wait_stream(stream)
+        with torch.cuda.graph(graph, stream=cap):
+            forward_into(x_full, cfg.m0, cfg.m1, out, prec=prec, stream=cap)
+        stream.wait_stream(cap)
         for _ in range(2):
             graph.replay()
         torch.cuda.synchronize()
@@ -317,6 +320,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                      "frac": achieved / peak, "traffic": ncu_traffic(cfg.name),
                      "peak_source": peak_src,
                      "bytes_per_launch": bytes_alg, "kernel_ms": kern_s * 1e3},
+        "kernel": dict(_lib.stream_kernel_info(cfg.m0, cfg.m1, prec), name="K1 k1_stream_kernel"),
         "clocks": clk.summary(),
         "gpu_launches": args.steps,
     }

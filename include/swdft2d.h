@@ -108,6 +108,11 @@ int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t
 /* Whether K1 is instantiated for (m0, m1, prec): 1 yes, 0 no. */
 int swdft2d_has_stream_kernel(int m0, int m1, int prec);
 
+/* Static shape of the K1 instantiation for (m0, m1, prec):
+ * info = {Q (J = 2^Q residue groups), TP1 (window columns per CTA), threads per CTA,
+ *         dynamic shared memory bytes}.  SWDFT2D_E_UNSUPPORTED if not instantiated. */
+int swdft2d_stream_kernel_info(int m0, int m1, int prec, int64_t info[4]);
+
 /*
  * Window-row strip partition for world ranks (single box):
  * rank g of G gets window rows [floor(P0*g/G), floor(P0*(g+1)/G)) and input rows

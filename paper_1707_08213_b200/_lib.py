@@ -42,6 +42,7 @@ SIGNATURES = {
     "swdft2d_forward": (_int, [_vp, _int, _i64, _i64, _i64, _int, _int, _int, _dbl, _i64, _i64,
                                _vp, _int, _vp]),
     "swdft2d_has_stream_kernel": (_int, [_int, _int, _int]),
+    "swdft2d_stream_kernel_info": (_int, [_int, _int, _int, _pi64]),
     "swdft2d_strip_range": (_int, [_i64, _int, _int, _int, _pi64]),
     "swdft2d_shutdown": (_int, []),
 }
@@ -114,3 +115,10 @@ def twiddles(n: int):
 
 def has_stream_kernel(m0: int, m1: int, prec: int) -> bool:
     return bool(load().swdft2d_has_stream_kernel(m0, m1, prec))
+
+
+def stream_kernel_info(m0: int, m1: int, prec: int) -> dict:
+    buf = (ctypes.c_int64 * 4)()
+    check(load().swdft2d_stream_kernel_info(m0, m1, prec, buf))
+    return {"Q": int(buf[0]), "J": 1 << int(buf[0]), "TP1": int(buf[1]), "threads": int(buf[2]),
+            "smem_bytes": int(buf[3])}

@@ -231,6 +231,17 @@ int swdft2d_twiddles(int n, double *out) {
 
 int swdft2d_has_stream_kernel(int m0, int m1, int prec) { return find_k1(m0, m1, prec) ? 1 : 0; }
 
+int swdft2d_stream_kernel_info(int m0, int m1, int prec, int64_t info[4]) {
+    const K1Info *k = find_k1(m0, m1, prec);
+    if (!k) return fail(SWDFT2D_E_UNSUPPORTED, "no K1 instantiation for m0=%d m1=%d prec=%d", m0, m1, prec);
+    if (!info) return fail(SWDFT2D_E_INVALID_ARG, "null info");
+    info[0] = k->q;
+    info[1] = k->tp1;
+    info[2] = k->threads;
+    info[3] = (int64_t)k->smem_bytes;
+    return SWDFT2D_OK;
+}
+
 int swdft2d_strip_range(int64_t P0, int m0, int rank, int world, int64_t range[4]) {
     if (world < 1 || rank < 0 || rank >= world || P0 < 0 || m0 < 0 || m0 > 62 || !range)
         return fail(SWDFT2D_E_INVALID_ARG, "bad strip request (P0=%lld rank=%d world=%d)",
