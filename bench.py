@@ -200,7 +200,7 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     from paper_1707_08213_b200 import WindowSpec, tree_swdft_2d
     from paper_1707_08213_b200 import _lib
-    from paper_1707_08213_b200.partition import strip_plan
+    from paper_1707_08213_b200.partition import scatter_strips, strip_plan
     from paper_1707_08213_b200.tree2d import _OUT_DTYPES, _precision_code, forward_into
 
     torch.cuda.set_device(local_rank)
@@ -223,18 +223,12 @@ def run_ours(args, cfg, rank, world, local_rank):
     recv = None if rank == 0 else torch.empty((re - rb, cfg.N1), dtype=xdt, device=dev)
 
     def step():
-        # scatter (N > 1): rank 0 -> every other rank, one batched NCCL group
+        # N > 1: the partitioner's scatter (one batched NCCL group of sends from rank 0)
         if world > 1:
-            ops = []
-            if rank == 0:
-                for g, (_, _, gb, ge) in enumerate(plan):
-                    if g and ge > gb:
-                        ops.append(dist.P2POp(dist.isend, x_full[gb:ge], g))
-            elif re > rb:
-                ops.append(dist.P2POp(dist.irecv, recv, 0))
-            for req in dist.batch_isend_irecv(ops) if ops else []:
-                req.wait()
-        src = x_full[rb:re] if rank == 0 else recv
+            src, _ = scatter_strips(x_full if rank == 0 else None, (cfg.N0, cfg.N1), cfg.m0, xdt,
+                                    dev, recv=recv)
+        else:
+            src = x_full
         if b > a:
             forward_into(src, cfg.m0, cfg.m1, out, prec=prec, stream=stream)
 

@@ -54,12 +54,13 @@ class ShardedCoefficients:
     normalization: str = "none"
 
 
-def scatter_strips(x, shape, m0: int, dtype, device, group=None, src: int = 0):
+def scatter_strips(x, shape, m0: int, dtype, device, group=None, src: int = 0, recv=None):
     """Scatter input row strips (with halos) from ``src``.
 
     ``x`` (a tensor on ``device``, rows contiguous) is only read on ``src``; the
-    other ranks pass None.  Returns (local_rows_tensor, (p0_begin, p0_end,
-    row_begin, row_end)).  Empty strips (P0 < world) come back as 0-row tensors.
+    other ranks pass None (and may pass a preallocated ``recv`` buffer of their
+    strip's shape).  Returns (local_rows_tensor, (p0_begin, p0_end, row_begin,
+    row_end)).  Empty strips (P0 < world) come back as 0-row tensors.
     """
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
@@ -76,7 +77,10 @@ def scatter_strips(x, shape, m0: int, dtype, device, group=None, src: int = 0):
                 ops.append(dist.P2POp(dist.isend, x[rb:re].contiguous(), g, group))
         local = x[my[2]:my[3]]
     else:
-        local = torch.empty((my[3] - my[2], N1), dtype=dtype, device=device)
+        local = recv if recv is not None else torch.empty((my[3] - my[2], N1), dtype=dtype,
+                                                          device=device)
+        if tuple(local.shape) != (my[3] - my[2], N1):
+            raise ValueError(f"recv buffer must have shape {(my[3] - my[2], N1)}")
         if my[3] > my[2]:
             ops.append(dist.P2POp(dist.irecv, local, src, group))
     if ops:
