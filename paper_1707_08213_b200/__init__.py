@@ -6,13 +6,13 @@ Drop-in for the reference's batch path ``swdft.tree2d.tree_swdft_2d``
 this package is the host-side mirror of the reference's interface plus the
 multi-GPU strip partitioner.
 """
-from .core import (BudgetError, CoefficientArray, DeviceError, InvalidWindowError, OpCounter,
+from .core import (BudgetError, CoefficientArray, ContainerError, DeviceError, InvalidWindowError, OpCounter,
                    ShapeError, StateError, SwdftError, UnsupportedError, WindowSpec,
                    WindowTooLargeError, normalization_factor)
 from .tree2d import LOOP_ORDERS, forward_into, tree_swdft_2d
 
 __all__ = [
-    "BudgetError", "CoefficientArray", "DeviceError", "InvalidWindowError", "OpCounter",
+    "BudgetError", "CoefficientArray", "ContainerError", "DeviceError", "InvalidWindowError", "OpCounter",
     "ShapeError", "StateError", "SwdftError", "UnsupportedError", "WindowSpec",
     "WindowTooLargeError", "normalization_factor", "LOOP_ORDERS", "forward_into",
     "tree_swdft_2d",

@@ -37,6 +37,10 @@ class StateError(SwdftError, RuntimeError):
     """Operation applied out of order (core.py:39)."""
 
 
+class ContainerError(SwdftError, ValueError):
+    """Malformed SWDF container, bad CSV, or non-finite payload (core.py:44)."""
+
+
 class BudgetError(SwdftError):
     """Projected allocation exceeds the configured memory budget (core.py:48-56)."""
 

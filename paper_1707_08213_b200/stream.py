@@ -1,0 +1,113 @@
+"""Row-push streaming form of the 2D tree SWDFT on the GPU.
+
+Mirror of the reference's ``tree2d.SlidingRowStream2D``
+(/root/reference/pkg/src/swdft/tree2d.py:205-303): push one
+length-N1 row at a time; once n0 rows have arrived every push returns the
+(P1, n0, n1) coefficient slab of the newest window row, and the slab sequence
+equals the batch transform's rows exactly.  The reference's
+implementation raises for every window larger than 1x1;
+this one implements the specified behaviour.
+
+Device state: the last n0 input rows in a double-stored ring (row p lives at
+slots p mod n0 and p mod n0 + n0), so the n0 rows a window row needs are always
+one contiguous [n0, N1] view; each push with p0 >= n0 - 1 runs the K1 kernel
+over that view for exactly one window row (bitwise equal to the batch output
+in fp64).  Operation accounting (``ops_last_push``, ``last_push_position_ops``,
+``counter.add_region``) follows tree2d.py:251-293 call for call.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib, core
+from .tree2d import _OUT_DTYPES, _precision_code, forward_into
+
+_RING_DTYPES = {_lib.PREC_FP32: torch.complex64, _lib.PREC_FP64: torch.complex128}
+
+
+class SlidingRowStream2D:
+    """Row-push streaming 2D tree SWDFT (tree2d.py:205-303 interface)."""
+
+    def __init__(self, spec, row_length: int, counter=None, *, precision="fp64", device=None,
+                 kernel: str = "auto"):
+        if len(spec.exponents) != 2:
+            raise core.ShapeError("SlidingRowStream2D needs a 2D window spec")
+        self.spec = spec
+        self.m0, self.m1 = (int(m) for m in spec.exponents)
+        self.n0, self.n1 = 1 << self.m0, 1 << self.m1
+        self.N1 = int(row_length)
+        if self.n1 > self.N1:
+            raise core.WindowTooLargeError(
+                f"window size {self.n1} exceeds row length {self.N1}")
+        self.counter = counter
+        self.prec = _precision_code(precision, None)
+        self.device = torch.device(device) if device is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+        self.kernel = kernel
+        self._factor = core.normalization_factor(spec)
+        self._ring = torch.zeros((2 * self.n0, self.N1), dtype=_RING_DTYPES[self.prec],
+                                 device=self.device)
+        self.P1 = self.N1 - self.n1 + 1
+        self._levels = self._level_plan()
+        self.rows_pushed = 0
+        self.ops_last_push = 0
+        self.last_push_position_ops = np.zeros(self.N1, dtype=np.int64)
+        self.closed = False
+
+    def _level_plan(self):
+        """(dim, shift, nodes) per tree level, core.shift_schedule order (core.py:197-220)."""
+        plan = []
+        for t in range(1, self.m1 + 1):
+            plan.append((1, 1 << (self.m1 - t), 1 << t))
+        for q in range(1, self.m0 + 1):
+            plan.append((0, 1 << (self.m0 - q), (1 << q) * self.n1))
+        return plan
+
+    def push_row(self, row):
+        """Ingest one length-N1 row; returns the (P1, n0, n1) slab (device tensor)
+        once n0 rows have arrived, None while warming up."""
+        if self.closed:
+            raise core.StateError("push after close")
+        if isinstance(row, torch.Tensor):
+            r = row
+        else:
+            r = torch.from_numpy(np.asarray(row, dtype=np.complex128))
+        if tuple(r.shape) != (self.N1,):
+            raise core.ShapeError(f"row shape {tuple(r.shape)} != ({self.N1},)")
+        p0 = self.rows_pushed
+        slot = p0 % self.n0
+        r = r.to(device=self.device, dtype=self._ring.dtype)
+        self._ring[slot].copy_(r)
+        self._ring[slot + self.n0].copy_(r)
+        # operation accounting, tree2d.py:251-293
+        self.last_push_position_ops[:] = 0
+        ops = 0
+        n0, n1, N1 = self.n0, self.n1, self.N1
+        for dim, s, nodes in self._levels:
+            if dim == 1:
+                lo = n1 - s
+                ops += (N1 - lo) * nodes
+                self.last_push_position_ops[lo:] += nodes
+                if self.counter is not None:
+                    self.counter.add_region((p0, slice(lo, N1)), nodes, N1 - lo)
+            else:
+                if p0 < n0 - s:
+                    break  # deeper column levels need even more rows
+                ops += (N1 - n1 + 1) * nodes
+                self.last_push_position_ops[n1 - 1:] += nodes
+                if self.counter is not None:
+                    self.counter.add_region((p0, slice(n1 - 1, N1)), nodes, N1 - n1 + 1)
+        self.ops_last_push = ops
+        self.rows_pushed += 1
+        if p0 < n0 - 1:
+            return None
+        first = (p0 + 1) % n0
+        window_rows = self._ring[first:first + n0]
+        slab = torch.empty((1, self.P1, n0, n1), dtype=_OUT_DTYPES[self.prec], device=self.device)
+        forward_into(window_rows, self.m0, self.m1, slab, prec=self.prec, scale=self._factor,
+                     kernel=self.kernel)
+        return slab[0]
+
+    def close(self) -> None:
+        self.closed = True

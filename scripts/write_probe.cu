@@ -31,6 +31,32 @@ __global__ void k1pattern(float4 *p, size_t n, size_t stride, size_t nblk_per_ro
     }
 }
 
+// TMA bulk store: each CTA stages CH bytes in shared memory (double-buffered) and one
+// thread issues cp.async.bulk.global.shared::cta for the whole chunk.
+template <int CH>
+__global__ void bulkstore(float4 *p, size_t n) {
+    extern __shared__ __align__(128) float4 sbuf[];  // 2 * CH bytes
+    const size_t per_chunk = CH / 16, nchunks = n / per_chunk;
+    int it = 0;
+    for (size_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
+        float4 *buf = sbuf + (it & 1) * per_chunk;
+        if (threadIdx.x == 0)  // buffer (it & 1) was last used two chunks ago
+            asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncthreads();
+        for (int i = threadIdx.x; i < (int)per_chunk; i += blockDim.x)
+            buf[i] = make_float4((float)i, (float)c, 2.f, 3.f);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned sa = (unsigned)__cvta_generic_to_shared(buf);
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                         :: "l"(p + c * per_chunk), "r"(sa), "r"(CH) : "memory");
+            asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+    }
+    if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 int main() {
     size_t bytes = 32ull << 30, n = bytes / 16;
     float4 *p;
@@ -38,6 +64,28 @@ int main() {
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
     const size_t stride = (33ull << 20) / 16, nblk = stride / 2048;
+    {
+        auto k = bulkstore<32768>;
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+        auto k2 = bulkstore<16384>;
+        for (int occ : {1, 2, 3}) {
+            float best = 1e30f, best2 = 1e30f;
+            for (int rep = 0; rep < 4; ++rep) {
+                cudaEventRecord(a);
+                k<<<sms * occ, 256, 65536>>>(p, n);
+                cudaEventRecord(b); cudaEventSynchronize(b);
+                float ms; cudaEventElapsedTime(&ms, a, b);
+                if (ms < best) best = ms;
+                cudaEventRecord(a);
+                k2<<<sms * occ * 2, 256, 32768>>>(p, n);
+                cudaEventRecord(b); cudaEventSynchronize(b);
+                cudaEventElapsedTime(&ms, a, b);
+                if (ms < best2) best2 = ms;
+            }
+            printf("{\"mode\": \"bulkstore32K\", \"ctas_per_sm\": %d, \"GBps\": %.1f}\n", occ, bytes / best / 1e6);
+            printf("{\"mode\": \"bulkstore16K\", \"ctas_per_sm\": %d, \"GBps\": %.1f}\n", occ * 2, bytes / best2 / 1e6);
+        }
+    }
     for (int mode = 0; mode < 4; ++mode)
         for (int occ : {2, 4, 8}) {
             float best = 1e30f;

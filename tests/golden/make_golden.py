@@ -165,6 +165,51 @@ def main():
         meta["budget"]["error"] = {"required": e.required_bytes, "budget": e.budget_bytes,
                                    "msg": str(e)}
 
+    # --- next rows: container bytes, 1D tree, 1x1 stream, verify, bench ops
+    from swdft import cli as ref_cli  # noqa: E402
+    from swdft import container as ref_container  # noqa: E402
+    from swdft import tree1d as ref_tree1d  # noqa: E402
+    import tempfile
+
+    nxt = {}
+    with tempfile.TemporaryDirectory() as td:
+        x = np.random.default_rng(21).standard_normal((12, 9))
+        out = ref_tree2d.tree_swdft_2d(x, ref_core.WindowSpec((2, 1), "unitary"))
+        pth = os.path.join(td, "c.swdf")
+        ref_container.write_swdf(pth, out.values, normalization=out.normalization)
+        nxt["swdf_unitary_12x9_w4x2"] = hashlib.sha256(open(pth, "rb").read()).hexdigest()
+        ref_container.write_swdf(pth, x)
+        nxt["swdf_real_12x9"] = hashlib.sha256(open(pth, "rb").read()).hexdigest()
+        # cmd_verify on a CSV input, normal and --corrupt (exit code + printed line)
+        csvp = os.path.join(td, "x.csv")
+        np.savetxt(csvp, x, delimiter=",")
+        import contextlib
+        import io as _io
+        res = {}
+        for flag in ([], ["--corrupt"]):
+            buf = _io.StringIO()
+            with contextlib.redirect_stdout(buf):
+                rc = ref_cli.main(["verify", "--input", csvp, "--window", "4x2"] + flag)
+            res["corrupt" if flag else "plain"] = {"rc": rc, "line": buf.getvalue().strip()}
+        nxt["verify"] = res
+    sigs = []
+    for i, (N, m) in enumerate([(40, 3), (17, 4), (9, 0), (64, 6)]):
+        s1 = np.random.default_rng(300 + i).standard_normal(N) + 1j * np.random.default_rng(400 + i).standard_normal(N)
+        c = ref_bench.OpCounter((N,))
+        v = ref_tree1d.tree_swdft_1d(s1, ref_core.WindowSpec((m,)), counter=c).values
+        sigs.append({"N": N, "m": m, "seed_re": 300 + i, "seed_im": 400 + i, "sha": sha(v),
+                     "total": int(c.total), "pos_sha": sha(c.position_ops)})
+    nxt["tree1d"] = sigs
+    # the reference stream works for 1x1 windows only (App. A #11)
+    xs = np.random.default_rng(55).standard_normal((7, 6))
+    st = ref_tree2d.SlidingRowStream2D(ref_core.WindowSpec((0, 0)), 6)
+    slabs = [st.push_row(r) for r in xs]
+    nxt["stream_1x1_sha"] = sha(np.stack(slabs))
+    nxt["fig4_predict_ops"] = {f"{w}": {a: int(ref_bench.predict_ops(a, (100, 100), (w, w)))
+                                        for a in ("tree", "fft", "naive")}
+                               for w in (4, 8, 16, 32, 64)}
+    meta["next"] = nxt
+
     # --- twiddles
     meta["twiddles"] = {str(1 << k): sha(ref_core.make_twiddles(1 << k)) for k in range(13)}
 
