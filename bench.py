@@ -206,7 +206,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
     spec = WindowSpec((cfg.m0, cfg.m1))
-    prec = _precision_code(cfg.precision, None)
+    prec = _precision_code(args.precision or cfg.precision, None)
     odt = _OUT_DTYPES[prec]
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
@@ -275,7 +275,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         t_job = t_local
     step_s = t_job / args.steps
     value = cfg.coefficients / step_s
-    bytes_alg = cfg.algorithmic_bytes()
+    out_bpc = 8 if prec == _lib.PREC_FP32 else 16
+    bytes_alg = cfg.coefficients * out_bpc + cfg.in_bytes
 
     # kernel-only number for the roofline: the single K1 launch of one step (N=1)
     kern_s = step_s
@@ -295,7 +296,8 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     peak, peak_src = measured_peak()
     achieved = bytes_alg / kern_s / 1e9 if world == 1 else (
-        cfg.algorithmic_bytes(rows=b - a) / (t_local / args.steps) / 1e9)
+        ((b - a) * P1 * n0 * n1 * out_bpc + (re - rb) * cfg.N1 * np.dtype(cfg.dtype).itemsize)
+        / (t_local / args.steps) / 1e9)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -305,11 +307,11 @@ def run_ours(args, cfg, rank, world, local_rank):
         "data": "synthetic (seeded, BASELINE.json recipe; see paper_1707_08213_b200/workloads.py)",
         "config": {"workload": cfg.name, "desc": cfg.desc, "N0": cfg.N0, "N1": cfg.N1,
                    "window": [n0, n1], "coefficients": cfg.coefficients,
-                   "output_bytes": cfg.coefficients * cfg.out_bytes_per_coef,
+                   "output_bytes": cfg.coefficients * out_bpc,
                    "l2": "256 MiB flush write between timed steps (outside the events); "
                          "output >> L2 as well",
                    "parallelism": f"strips{world}" if world > 1 else "single"},
-        "hbm_write_gbs": cfg.coefficients * cfg.out_bytes_per_coef / step_s / 1e9,
+        "hbm_write_gbs": cfg.coefficients * out_bpc / step_s / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": ncu_traffic(cfg.name),
                      "peak_source": peak_src,
@@ -374,6 +376,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--precision", default=None, choices=[None, "fp32", "fp64"],
+                    help="override the config's precision (fp64 = DAG-exact complex128)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 

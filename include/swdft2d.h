@@ -110,8 +110,10 @@ int swdft2d_has_stream_kernel(int m0, int m1, int prec);
 
 /* Static shape of the K1 instantiation for (m0, m1, prec):
  * info = {Q (J = 2^Q residue groups), TP1 (window columns per CTA), threads per CTA,
- *         dynamic shared memory bytes}.  SWDFT2D_E_UNSUPPORTED if not instantiated. */
-int swdft2d_stream_kernel_info(int m0, int m1, int prec, int64_t info[4]);
+ *         dynamic shared memory bytes (LDG variant), rows per batch NB,
+ *         1 if the TMA input-staging variant is used for TMA-addressable inputs}.
+ * SWDFT2D_E_UNSUPPORTED if not instantiated. */
+int swdft2d_stream_kernel_info(int m0, int m1, int prec, int64_t info[6]);
 
 /*
  * Window-row strip partition for world ranks (single box):

@@ -118,7 +118,7 @@ def has_stream_kernel(m0: int, m1: int, prec: int) -> bool:
 
 
 def stream_kernel_info(m0: int, m1: int, prec: int) -> dict:
-    buf = (ctypes.c_int64 * 4)()
+    buf = (ctypes.c_int64 * 6)()
     check(load().swdft2d_stream_kernel_info(m0, m1, prec, buf))
     return {"Q": int(buf[0]), "J": 1 << int(buf[0]), "TP1": int(buf[1]), "threads": int(buf[2]),
-            "smem_bytes": int(buf[3])}
+            "smem_bytes_ldg": int(buf[3]), "NB": int(buf[4]), "tma_input_staging": bool(buf[5])}

@@ -8,11 +8,14 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
 #include <string>
 #include <utility>
+
+#include <cudaTypedefs.h>
 
 #include "../../include/swdft2d.h"
 #include "swdft2d_internal.h"
@@ -28,6 +31,11 @@ void k1_register_m0_5();
 void k1_register_m0_6();
 
 static thread_local std::string g_last_error;
+// TMA input staging on by default; SWDFT2D_TMA=0 selects the register-prefetch (LDG) variant.
+static const bool g_use_tma = [] {
+    const char *e = std::getenv("SWDFT2D_TMA");
+    return !(e && e[0] == '0');
+}();
 
 static int fail(int code, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
 static int fail(int code, const char *fmt, ...) {
@@ -41,9 +49,9 @@ static int fail(int code, const char *fmt, ...) {
 }
 
 // ---- K1 registry ---------------------------------------------------------
-static const K1Info *g_k1[SWDFT2D_K1_MAX_M + 1][SWDFT2D_K1_MAX_M + 1][2];
+static const K1Info *g_k1[SWDFT2D_K1_MAX_M + 1][SWDFT2D_K1_MAX_M + 1][2][2];  // [m0][m1][prec][tma]
 
-void register_k1(const K1Info *info) { g_k1[info->m0][info->m1][info->prec] = info; }
+void register_k1(const K1Info *info) { g_k1[info->m0][info->m1][info->prec][info->tma] = info; }
 
 static void ensure_registered() {
     static std::once_flag once;
@@ -58,11 +66,58 @@ static void ensure_registered() {
     });
 }
 
-const K1Info *find_k1(int m0, int m1, int prec) {
+const K1Info *find_k1(int m0, int m1, int prec, int tma) {
     ensure_registered();
-    if (m0 < 0 || m1 < 0 || m0 > SWDFT2D_K1_MAX_M || m1 > SWDFT2D_K1_MAX_M || prec < 0 || prec > 1)
+    if (m0 < 0 || m1 < 0 || m0 > SWDFT2D_K1_MAX_M || m1 > SWDFT2D_K1_MAX_M || prec < 0 ||
+        prec > 1 || tma < 0 || tma > 1)
         return nullptr;
-    return g_k1[m0][m1][prec];
+    return g_k1[m0][m1][prec][tma];
+}
+
+// ---- TMA tensor map for the input (driver entry point, no libcuda link) -----
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }();
+    return fn;
+}
+
+// Describes x as a 2D tensor of 4- or 8-byte elements (complex128 = 2 elements per
+// sample); box = NB rows x (TP1 + n1 - 1) samples rounded up to 16 B.  Returns false
+// when TMA cannot address x (alignment, strides, box limits): the LDG path is used.
+static bool encode_input_map(const K1Info *k, const void *x, int in_dtype, int64_t N0, int64_t N1,
+                             int64_t ldx, CUtensorMap *map, K1Params *P) {
+    static const int sample_bytes[4] = {4, 8, 8, 16};
+    const int sb = sample_bytes[in_dtype];
+    const int elt = in_dtype == SWDFT2D_IN_F32 ? 4 : 8;
+    const int per = sb / elt;
+    const int n1 = 1 << k->m1;
+    const int row_bytes = ((k->tp1 + n1 - 1) * sb + 15) / 16 * 16;
+    const int box_w = row_bytes / elt;
+    P->sample_bytes = sb;
+    P->tma_per_sample = per;
+    P->tma_row_bytes = row_bytes;
+    if (((uintptr_t)x & 15) || ((ldx * sb) & 15) || box_w > 256 || k->nb > 256 ||
+        N0 > 0x7fffffffLL || N1 * per > 0xffffffffLL)
+        return false;
+    auto fn = encode_fn();
+    if (!fn) return false;
+    const CUtensorMapDataType dt =
+        in_dtype == SWDFT2D_IN_F32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT64;
+    const cuuint64_t gdim[2] = {(cuuint64_t)(N1 * per), (cuuint64_t)N0};
+    const cuuint64_t gstride[1] = {(cuuint64_t)(ldx * sb)};
+    const cuuint32_t box[2] = {(cuuint32_t)box_w, (cuuint32_t)k->nb};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, dt, 2, const_cast<void *>(x), gdim, gstride, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
 }
 
 // ---- per-device state ----------------------------------------------------
@@ -239,6 +294,8 @@ int swdft2d_stream_kernel_info(int m0, int m1, int prec, int64_t info[4]) {
     info[1] = k->tp1;
     info[2] = k->threads;
     info[3] = (int64_t)k->smem_bytes;
+    info[4] = k->nb;
+    info[5] = (g_use_tma && find_k1(m0, m1, prec, 1)) ? 1 : 0;
     return SWDFT2D_OK;
 }
 
@@ -282,14 +339,20 @@ int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t
     const int n0 = 1 << m0;
     const bool apply = !(scale == 1.0);
 
-    const K1Info *k1 = find_k1(m0, m1, prec);
+    const K1Info *k1 = find_k1(m0, m1, prec, 0);
     if (kernel == SWDFT2D_KERNEL_STREAM && !k1)
         return fail(SWDFT2D_E_UNSUPPORTED, "no K1 instantiation for m0=%d m1=%d prec=%d", m0, m1, prec);
     if (kernel != SWDFT2D_KERNEL_WINDOW && k1) {
-        int occ = 0;
-        if ((rc = k1_occupancy(ds, k1, &occ))) return rc;
         K1Params P;
         std::memset(&P, 0, sizeof P);
+        CUtensorMap tmap;
+        std::memset(&tmap, 0, sizeof tmap);
+        // the TMA variant stages input tiles with cp.async.bulk.tensor when x is addressable
+        const K1Info *kt = g_use_tma ? find_k1(m0, m1, prec, 1) : nullptr;
+        if (kt && encode_input_map(kt, x, in_dtype, N0, N1, ld_x, &tmap, &P)) k1 = kt;
+        else encode_input_map(k1, x, in_dtype, N0, N1, ld_x, &tmap, &P);  // fills sample_bytes
+        int occ = 0;
+        if ((rc = k1_occupancy(ds, k1, &occ))) return rc;
         P.x = x;
         P.in_dtype = in_dtype;
         P.apply_scale = apply ? 1 : 0;
@@ -310,7 +373,7 @@ int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t
         host_twiddles(K1_TW_N, re, im);
         for (int i = 0; i < K1_TW_N; ++i) P.tw[i] = make_double2(re[i], im[i]);
         const int64_t grid = P.ntiles < slots ? P.ntiles : slots;
-        k1->launch(P, (int)grid, st);
+        k1->launch(P, tmap, (int)grid, st);
     } else {
         if (m0 > SWDFT2D_K0_MAX_M || m1 > SWDFT2D_K0_MAX_M)
             return fail(SWDFT2D_E_UNSUPPORTED, "window 2^%d x 2^%d exceeds the CUDA paths (max 2^%d)",

@@ -39,6 +39,8 @@
 #include <type_traits>
 #include <utility>
 
+#include <cuda.h>
+
 #include "swdft2d_device.cuh"
 #include "swdft2d_internal.h"
 
@@ -78,35 +80,58 @@ template <int M0, int M1, int Q, int TP1, int NBM = 1> struct K1Shape {
     static constexpr int RING = cmax((M0 - Q) * (n0 / (2 * J)), 1);  // register ring, complex
     static constexpr int OUTS = n0 / J;                   // coefficients per thread per row
     static constexpr int UNR = cmin(cmax(n0 / (2 * J), 8), NB);  // stage-C rows per unrolled block
+    // TMA staging: 2 stages x NB rows x (TP1 + n1 - 1) samples of <= 16 B, rows 16-B padded
+    static constexpr int STAGE_ROW_MAX = ((TP1 + n1 - 1) * 16 + 15) / 16 * 16;
+    static constexpr int STAGE_SPAN = (NB * STAGE_ROW_MAX + 127) / 128 * 128;  // 128-B aligned
+    static constexpr int STAGE_BYTES = 2 * STAGE_SPAN;
     static_assert(Q <= M0, "J must divide n0");
     static_assert(NT % 32 == 0 && NT <= 1024, "CTA size must be a warp multiple <= 1024");
 };
 
-template <typename T, int M0, int M1, int Q, int TP1, int NBM = 1>
+template <typename T, int M0, int M1, int Q, int TP1, int NBM = 1, bool TMA = false>
 constexpr size_t k1_smem_bytes() {
     using S = K1Shape<M0, M1, Q, TP1, NBM>;
-    return sizeof(cplx<T>) * ((size_t)S::D * TP1 * S::n1 + S::NMAX);
+    return (TMA ? (size_t)S::STAGE_BYTES : 0) +
+           sizeof(cplx<T>) * ((size_t)S::D * TP1 * S::n1 + S::NMAX);
 }
 
-template <typename T, int M0, int M1, int Q, int TP1, bool EXACT, int MINB = 1, int NBM = 1>
+template <typename T, int M0, int M1, int Q, int TP1, bool EXACT, int MINB = 1, int NBM = 1,
+          bool TMA = false>
 __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
-    k1_stream_kernel(const __grid_constant__ K1Params P) {
+    k1_stream_kernel(const __grid_constant__ K1Params P, const __grid_constant__ CUtensorMap tmap) {
     using S = K1Shape<M0, M1, Q, TP1, NBM>;
     using C = cplx<T>;
     constexpr int n0 = S::n0, n1 = S::n1, J = S::J, NB = S::NB, D = S::D;
     constexpr int G = S::G, V = S::V, GW = S::GW, TPR = S::TPR, NMAX = S::NMAX;
     constexpr int ST0 = NMAX / n0, ST1 = NMAX / n1;  // table strides (exact, App. A #4)
 
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    C *ring = reinterpret_cast<C *>(smem_raw);  // [D][TP1][n1]
-    C *tw = ring + D * TP1 * n1;                // make_twiddles(NMAX)
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    unsigned char *stage = smem_raw;  // TMA: 2 x [NB][row] input tiles (128-B aligned)
+    C *ring = reinterpret_cast<C *>(smem_raw + (TMA ? S::STAGE_BYTES : 0));  // [D][TP1][n1]
+    C *tw = ring + D * TP1 * n1;                                             // make_twiddles(NMAX)
+    __shared__ __align__(8) uint64_t mbar[2];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int i = tid; i < NMAX; i += S::NT) {
         const double2 w = P.tw[i * (K1_TW_N / NMAX)];
         tw[i] = mk<T>((T)w.x, (T)w.y);
     }
+    if constexpr (TMA) {
+        if (tid == 0) {
+            mbar_init(&mbar[0], 1);
+            mbar_init(&mbar[1], 1);
+            fence_mbar_init();
+            asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
+        }
+    }
     __syncthreads();
+    // TMA: one elected thread loads batch gb's [NB x box] input tile into stage gb & 1
+    uint32_t gb = 0;  // batches processed by this CTA (mbarrier phase bookkeeping)
+    auto tma_issue = [&](uint32_t g, int64_t brow, int64_t pbase) {
+        mbar_expect_tx(&mbar[g & 1], (uint32_t)(NB * P.tma_row_bytes));
+        tma_load_2d(stage + (g & 1) * S::STAGE_SPAN, &tmap, &mbar[g & 1],
+                    (int)(pbase * P.tma_per_sample), (int)brow);
+    };
 
     // stage C identity: column (pos, k1), output residue j
     const int k1 = tid % n1, j = (tid / n1) % J, pos = tid / (n1 * J);
@@ -149,9 +174,17 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
                 }
             }
         };
-        load_batch(0);
+        if constexpr (TMA) {
+            if (tid == 0) tma_issue(gb, r0, pbase);
+        } else {
+            load_batch(0);
+        }
 
-        for (int b = 0; b < nbatch; ++b) {
+        for (int b = 0; b < nbatch; ++b, ++gb) {
+            if constexpr (TMA) {
+                if (tid == 0 && b + 1 < nbatch) tma_issue(gb + 1, r0 + (int64_t)(b + 1) * NB, pbase);
+                mbar_wait(&mbar[gb & 1], (gb >> 1) & 1);
+            }
             // ---------------- stage R: row transforms of NB rows into the ring
 #pragma unroll
             for (int tt = 0; tt < S::TPW; ++tt) {
@@ -160,8 +193,17 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
                     const int rr = task / TPR, pg = task - rr * TPR;
                     const int pl = pg * GW + gam;
                     C s[V];
+                    if constexpr (TMA) {
+                        const unsigned char *rowp =
+                            stage + (gb & 1) * S::STAGE_SPAN + rr * P.tma_row_bytes;
 #pragma unroll
-                    for (int a = 0; a < V; ++a) s[a] = xs[tt][a];
+                        for (int a = 0; a < V; ++a)
+                            s[a] = load_staged<T>(rowp + (pl + lam + G * a) * P.sample_bytes,
+                                                  P.in_dtype);
+                    } else {
+#pragma unroll
+                        for (int a = 0; a < V; ++a) s[a] = xs[tt][a];
+                    }
                     // in-register levels (n1 > 32): classes c = lam + G*a
 #pragma unroll
                     for (int L = 2; L <= V; L *= 2) {
@@ -205,7 +247,9 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
                 }
             }
             __syncthreads();
-            if (b + 1 < nbatch) load_batch(b + 1);
+            if constexpr (!TMA) {
+                if (b + 1 < nbatch) load_batch(b + 1);
+            }
             // ---------------- stage C: column trees, NB rows, UNR rows per unrolled block
             // (UNR is a multiple of every register-ring depth, so ring slots are static)
 #pragma unroll 1
@@ -271,22 +315,25 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
 }
 
 // Per-instantiation launcher + registry entry.
-template <typename T, int M0, int M1, int Q, int TP1, bool EXACT, int MINB = 1, int NBM = 1>
-int k1_launch(const K1Params &P, int grid, cudaStream_t stream) {
+template <typename T, int M0, int M1, int Q, int TP1, bool EXACT, int MINB = 1, int NBM = 1,
+          bool TMA = false>
+int k1_launch(const K1Params &P, const CUtensorMap &tmap, int grid, cudaStream_t stream) {
     using S = K1Shape<M0, M1, Q, TP1, NBM>;
-    constexpr size_t smem = k1_smem_bytes<T, M0, M1, Q, TP1, NBM>();
-    k1_stream_kernel<T, M0, M1, Q, TP1, EXACT, MINB, NBM><<<grid, S::NT, smem, stream>>>(P);
+    constexpr size_t smem = k1_smem_bytes<T, M0, M1, Q, TP1, NBM, TMA>();
+    k1_stream_kernel<T, M0, M1, Q, TP1, EXACT, MINB, NBM, TMA><<<grid, S::NT, smem, stream>>>(P, tmap);
     return 0;
 }
 
 // Registry entry for an explicit shape (used by K1Inst and by the tuning harness).
-template <typename T, int M0, int M1, int Q, int TP1, bool EXACT, int MINB = 1, int NBM = 1>
+template <typename T, int M0, int M1, int Q, int TP1, bool EXACT, int MINB = 1, int NBM = 1,
+          bool TMA = false>
 const K1Info *k1_info() {
     using S = K1Shape<M0, M1, Q, TP1, NBM>;
     static const K1Info info = {
-        M0, M1, EXACT ? 1 : 0, Q, TP1, S::NT, k1_smem_bytes<T, M0, M1, Q, TP1, NBM>(),
-        (const void *)&k1_stream_kernel<T, M0, M1, Q, TP1, EXACT, MINB, NBM>,
-        &k1_launch<T, M0, M1, Q, TP1, EXACT, MINB, NBM>};
+        M0, M1, EXACT ? 1 : 0, Q, TP1, S::NT, S::NB, TMA ? 1 : 0,
+        k1_smem_bytes<T, M0, M1, Q, TP1, NBM, TMA>(),
+        (const void *)&k1_stream_kernel<T, M0, M1, Q, TP1, EXACT, MINB, NBM, TMA>,
+        &k1_launch<T, M0, M1, Q, TP1, EXACT, MINB, NBM, TMA>};
     return &info;
 }
 
@@ -310,7 +357,10 @@ template <int M0, int M1, bool DBL> struct K1Inst {
     static constexpr int Q = k1_choose_q(M0, M1);
     static constexpr int TP1 = k1_choose_tp1(M1, Q);
     using S = K1Shape<M0, M1, Q, TP1>;
-    static void reg() { register_k1(k1_info<T, M0, M1, Q, TP1, DBL>()); }
+    static void reg() {
+        register_k1(k1_info<T, M0, M1, Q, TP1, DBL>());
+        register_k1(k1_info<T, M0, M1, Q, TP1, DBL, 1, 1, true>());
+    }
 };
 
 }  // namespace swdft2d

@@ -100,6 +100,60 @@ __device__ __forceinline__ cplx<T> load_x(const void *__restrict__ x, int in_dty
     }
 }
 
+// Sample of x staged in shared memory (TMA tile), element type in_dtype.
+template <typename T>
+__device__ __forceinline__ cplx<T> load_staged(const unsigned char *p, int in_dtype) {
+    switch (in_dtype) {
+    case 0: return mk<T>((T) * reinterpret_cast<const float *>(p), (T)0);
+    case 1: return mk<T>((T) * reinterpret_cast<const double *>(p), (T)0);
+    case 2: {
+        const float2 v = *reinterpret_cast<const float2 *>(p);
+        return mk<T>((T)v.x, (T)v.y);
+    }
+    default: {
+        const double2 v = *reinterpret_cast<const double2 *>(p);
+        return mk<T>((T)v.x, (T)v.y);
+    }
+    }
+}
+
+// ---- mbarrier + TMA (cp.async.bulk.tensor) helpers --------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+                 : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 2D tensor tile global -> shared, completion counted on `bar` (transaction bytes).
+__device__ __forceinline__ void tma_load_2d(void *dst, const void *tmap, uint64_t *bar, int x,
+                                            int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(tmap), "r"(smem_u32(bar)), "r"(x), "r"(y)
+        : "memory");
+}
+
 // Streaming (evict-first) 8/16-byte stores for the write-once coefficient output.
 __device__ __forceinline__ void st_stream(float2 *p, float2 v) { __stcs(p, v); }
 __device__ __forceinline__ void st_stream(double2 *p, double2 v) { __stcs(p, v); }

@@ -2,6 +2,7 @@
 // prototypes (internal to libswdft2d.so; the public surface is include/swdft2d.h).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -30,19 +31,22 @@ struct K1Params {
     int64_t CB;      // column blocks of TP1 window positions
     int64_t RCH;     // window rows per tile
     int64_t ntiles;  // CB * ceil(rows / RCH)
+    int sample_bytes;    // bytes per input sample (4, 8, 16)
+    int tma_per_sample;  // TMA elements per sample (1, or 2 for complex128)
+    int tma_row_bytes;   // bytes of one staged input row (TMA box width, 16-B multiple)
     double2 tw[K1_TW_N];
 };
 
 // Static shape of one K1 instantiation (filled by the instantiation units).
 struct K1Info {
-    int m0, m1, prec, q, tp1, threads;
+    int m0, m1, prec, q, tp1, threads, nb, tma;
     size_t smem_bytes;
     const void *func;  // kernel symbol for occupancy queries / attribute setting
-    int (*launch)(const K1Params &, int grid, cudaStream_t);
+    int (*launch)(const K1Params &, const CUtensorMap &, int grid, cudaStream_t);
 };
 
-// Registry of compiled K1 instantiations; nullptr if (m0, m1, prec) is absent.
-const K1Info *find_k1(int m0, int m1, int prec);
+// Registry of compiled K1 instantiations; nullptr if (m0, m1, prec, tma) is absent.
+const K1Info *find_k1(int m0, int m1, int prec, int tma = 0);
 void register_k1(const K1Info *info);
 
 int launch_k0(const K0Params &P, int prec, cudaStream_t stream);
