@@ -98,7 +98,8 @@ static bool encode_input_map(const K1Info *k, const void *x, int in_dtype, int64
     const int elt = in_dtype == SWDFT2D_IN_F32 ? 4 : 8;
     const int per = sb / elt;
     const int n1 = 1 << k->m1;
-    const int row_bytes = ((k->tp1 + n1 - 1) * sb + 15) / 16 * 16;
+    // + 16 B: the box starts at the 16-B boundary at or left of the tile's first sample
+    const int row_bytes = ((k->tp1 + n1 - 1) * sb + 15) / 16 * 16 + (sb < 16 ? 16 : 0);
     const int box_w = row_bytes / elt;
     P->sample_bytes = sb;
     P->tma_per_sample = per;

@@ -80,8 +80,9 @@ template <int M0, int M1, int Q, int TP1, int NBM = 1> struct K1Shape {
     static constexpr int RING = cmax((M0 - Q) * (n0 / (2 * J)), 1);  // register ring, complex
     static constexpr int OUTS = n0 / J;                   // coefficients per thread per row
     static constexpr int UNR = cmin(cmax(n0 / (2 * J), 8), NB);  // stage-C rows per unrolled block
-    // TMA staging: 2 stages x NB rows x (TP1 + n1 - 1) samples of <= 16 B, rows 16-B padded
-    static constexpr int STAGE_ROW_MAX = ((TP1 + n1 - 1) * 16 + 15) / 16 * 16;
+    // TMA staging: 2 stages x NB rows x (TP1 + n1 - 1) samples of <= 16 B, plus up to
+    // 16 B in front (the box starts on a 16-B aligned column), rows 16-B padded
+    static constexpr int STAGE_ROW_MAX = ((TP1 + n1 - 1) * 16 + 15) / 16 * 16 + 16;
     static constexpr int STAGE_SPAN = (NB * STAGE_ROW_MAX + 127) / 128 * 128;  // 128-B aligned
     static constexpr int STAGE_BYTES = 2 * STAGE_SPAN;
     static_assert(Q <= M0, "J must divide n0");
@@ -127,10 +128,15 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
     __syncthreads();
     // TMA: one elected thread loads batch gb's [NB x box] input tile into stage gb & 1
     uint32_t gb = 0;  // batches processed by this CTA (mbarrier phase bookkeeping)
+    // The box's first column must sit on a 16-byte boundary of the row (measured: an
+    // unaligned inner coordinate faults), so it starts `shift` samples left of pbase.
+    auto tma_shift = [&](int64_t pbase) {
+        return (int)(((pbase * P.sample_bytes) & 15) / P.sample_bytes);
+    };
     auto tma_issue = [&](uint32_t g, int64_t brow, int64_t pbase) {
         mbar_expect_tx(&mbar[g & 1], (uint32_t)(NB * P.tma_row_bytes));
         tma_load_2d(stage + (g & 1) * S::STAGE_SPAN, &tmap, &mbar[g & 1],
-                    (int)(pbase * P.tma_per_sample), (int)brow);
+                    (int)((pbase - tma_shift(pbase)) * P.tma_per_sample), (int)brow);
     };
 
     // stage C identity: column (pos, k1), output residue j
@@ -196,9 +202,10 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
                     if constexpr (TMA) {
                         const unsigned char *rowp =
                             stage + (gb & 1) * S::STAGE_SPAN + rr * P.tma_row_bytes;
+                        const int sh = tma_shift(pbase);
 #pragma unroll
                         for (int a = 0; a < V; ++a)
-                            s[a] = load_staged<T>(rowp + (pl + lam + G * a) * P.sample_bytes,
+                            s[a] = load_staged<T>(rowp + (sh + pl + lam + G * a) * P.sample_bytes,
                                                   P.in_dtype);
                     } else {
 #pragma unroll
