@@ -31,10 +31,12 @@ void k1_register_m0_5();
 void k1_register_m0_6();
 
 static thread_local std::string g_last_error;
-// TMA input staging on by default; SWDFT2D_TMA=0 selects the register-prefetch (LDG) variant.
+// K1 input path: register prefetch (LDG, default) or TMA tile staging (SWDFT2D_TMA=1).
+// Measured on B200 (profiles/TMA_r01.md): the input is ~0.2 % of the traffic and the
+// LDG variant is 3-12 % faster on configs 2-4 and level on config 5.
 static const bool g_use_tma = [] {
     const char *e = std::getenv("SWDFT2D_TMA");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
 }();
 
 static int fail(int code, const char *fmt, ...) __attribute__((format(printf, 2, 3)));

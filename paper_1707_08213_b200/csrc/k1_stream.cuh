@@ -84,7 +84,8 @@ template <int M0, int M1, int Q, int TP1, int NBM = 1> struct K1Shape {
     // 16 B in front (the box starts on a 16-B aligned column), rows 16-B padded
     static constexpr int STAGE_ROW_MAX = ((TP1 + n1 - 1) * 16 + 15) / 16 * 16 + 16;
     static constexpr int STAGE_SPAN = (NB * STAGE_ROW_MAX + 127) / 128 * 128;  // 128-B aligned
-    static constexpr int STAGE_BYTES = 2 * STAGE_SPAN;
+    static constexpr int NSTAGE = 4;  // TMA tiles in flight: batch b loads while b-3 computes
+    static constexpr int STAGE_BYTES = NSTAGE * STAGE_SPAN;
     static_assert(Q <= M0, "J must divide n0");
     static_assert(NT % 32 == 0 && NT <= 1024, "CTA size must be a warp multiple <= 1024");
 };
@@ -110,7 +111,7 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
     unsigned char *stage = smem_raw;  // TMA: 2 x [NB][row] input tiles (128-B aligned)
     C *ring = reinterpret_cast<C *>(smem_raw + (TMA ? S::STAGE_BYTES : 0));  // [D][TP1][n1]
     C *tw = ring + D * TP1 * n1;                                             // make_twiddles(NMAX)
-    __shared__ __align__(8) uint64_t mbar[2];
+    __shared__ __align__(8) uint64_t mbar[S::NSTAGE];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int i = tid; i < NMAX; i += S::NT) {
@@ -119,14 +120,13 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
     }
     if constexpr (TMA) {
         if (tid == 0) {
-            mbar_init(&mbar[0], 1);
-            mbar_init(&mbar[1], 1);
+            for (int i = 0; i < S::NSTAGE; ++i) mbar_init(&mbar[i], 1);
             fence_mbar_init();
             asm volatile("prefetch.tensormap [%0];" ::"l"(&tmap) : "memory");
         }
     }
     __syncthreads();
-    // TMA: one elected thread loads batch gb's [NB x box] input tile into stage gb & 1
+    // TMA: one elected thread loads batch gb's [NB x box] input tile into stage gb % NSTAGE
     uint32_t gb = 0;  // batches processed by this CTA (mbarrier phase bookkeeping)
     // The box's first column must sit on a 16-byte boundary of the row (measured: an
     // unaligned inner coordinate faults), so it starts `shift` samples left of pbase.
@@ -134,8 +134,9 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
         return (int)(((pbase * P.sample_bytes) & 15) / P.sample_bytes);
     };
     auto tma_issue = [&](uint32_t g, int64_t brow, int64_t pbase) {
-        mbar_expect_tx(&mbar[g & 1], (uint32_t)(NB * P.tma_row_bytes));
-        tma_load_2d(stage + (g & 1) * S::STAGE_SPAN, &tmap, &mbar[g & 1],
+        const int st = (int)(g % S::NSTAGE);
+        mbar_expect_tx(&mbar[st], (uint32_t)(NB * P.tma_row_bytes));
+        tma_load_2d(stage + st * S::STAGE_SPAN, &tmap, &mbar[st],
                     (int)((pbase - tma_shift(pbase)) * P.tma_per_sample), (int)brow);
     };
 
@@ -180,16 +181,20 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
                 }
             }
         };
+        const int tsh = TMA ? tma_shift(pbase) : 0;  // staged column of window column pbase
         if constexpr (TMA) {
-            if (tid == 0) tma_issue(gb, r0, pbase);
+            if (tid == 0)
+                for (int i = 0; i < S::NSTAGE - 1 && i < nbatch; ++i)
+                    tma_issue(gb + i, r0 + (int64_t)i * NB, pbase);
         } else {
             load_batch(0);
         }
 
         for (int b = 0; b < nbatch; ++b, ++gb) {
             if constexpr (TMA) {
-                if (tid == 0 && b + 1 < nbatch) tma_issue(gb + 1, r0 + (int64_t)(b + 1) * NB, pbase);
-                mbar_wait(&mbar[gb & 1], (gb >> 1) & 1);
+                if (tid == 0 && b + S::NSTAGE - 1 < nbatch)
+                    tma_issue(gb + S::NSTAGE - 1, r0 + (int64_t)(b + S::NSTAGE - 1) * NB, pbase);
+                mbar_wait(&mbar[gb % S::NSTAGE], (gb / S::NSTAGE) & 1);
             }
             // ---------------- stage R: row transforms of NB rows into the ring
 #pragma unroll
@@ -201,11 +206,10 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
                     C s[V];
                     if constexpr (TMA) {
                         const unsigned char *rowp =
-                            stage + (gb & 1) * S::STAGE_SPAN + rr * P.tma_row_bytes;
-                        const int sh = tma_shift(pbase);
+                            stage + (gb % S::NSTAGE) * S::STAGE_SPAN + rr * P.tma_row_bytes;
 #pragma unroll
                         for (int a = 0; a < V; ++a)
-                            s[a] = load_staged<T>(rowp + (sh + pl + lam + G * a) * P.sample_bytes,
+                            s[a] = load_staged<T>(rowp + (tsh + pl + lam + G * a) * P.sample_bytes,
                                                   P.in_dtype);
                     } else {
 #pragma unroll
