@@ -27,8 +27,9 @@ E_NOMEM = -8
 
 IN_F32, IN_F64, IN_C64, IN_C128 = 0, 1, 2, 3
 PREC_FP32, PREC_FP64 = 0, 1
-KERNEL_AUTO, KERNEL_STREAM, KERNEL_WINDOW = 0, 1, 2
-KERNELS = {"auto": KERNEL_AUTO, "stream": KERNEL_STREAM, "window": KERNEL_WINDOW}
+KERNEL_AUTO, KERNEL_STREAM, KERNEL_WINDOW, KERNEL_STREAM_TMA = 0, 1, 2, 3
+KERNELS = {"auto": KERNEL_AUTO, "stream": KERNEL_STREAM, "window": KERNEL_WINDOW,
+           "stream_tma": KERNEL_STREAM_TMA}
 
 # every symbol include/swdft2d.h declares: name -> (restype, argtypes)
 _i64, _int, _dbl, _vp = ctypes.c_int64, ctypes.c_int, ctypes.c_double, ctypes.c_void_p

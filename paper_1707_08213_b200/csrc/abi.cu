@@ -334,7 +334,7 @@ int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t
                     (long long)p0_begin, (long long)p0_end, (long long)P0);
     if (p0_begin == p0_end) return SWDFT2D_OK;
     if (!x || !out) return fail(SWDFT2D_E_INVALID_ARG, "null device pointer");
-    if (kernel < SWDFT2D_KERNEL_AUTO || kernel > SWDFT2D_KERNEL_WINDOW)
+    if (kernel < SWDFT2D_KERNEL_AUTO || kernel > SWDFT2D_KERNEL_STREAM_TMA)
         return fail(SWDFT2D_E_INVALID_ARG, "unknown kernel code %d", kernel);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     DeviceState *ds = nullptr;
@@ -343,7 +343,7 @@ int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t
     const bool apply = !(scale == 1.0);
 
     const K1Info *k1 = find_k1(m0, m1, prec, 0);
-    if (kernel == SWDFT2D_KERNEL_STREAM && !k1)
+    if ((kernel == SWDFT2D_KERNEL_STREAM || kernel == SWDFT2D_KERNEL_STREAM_TMA) && !k1)
         return fail(SWDFT2D_E_UNSUPPORTED, "no K1 instantiation for m0=%d m1=%d prec=%d", m0, m1, prec);
     if (kernel != SWDFT2D_KERNEL_WINDOW && k1) {
         K1Params P;
@@ -351,7 +351,9 @@ int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t
         CUtensorMap tmap;
         std::memset(&tmap, 0, sizeof tmap);
         // the TMA variant stages input tiles with cp.async.bulk.tensor when x is addressable
-        const K1Info *kt = g_use_tma ? find_k1(m0, m1, prec, 1) : nullptr;
+        const bool want_tma =
+            kernel == SWDFT2D_KERNEL_STREAM_TMA || (kernel == SWDFT2D_KERNEL_AUTO && g_use_tma);
+        const K1Info *kt = want_tma ? find_k1(m0, m1, prec, 1) : nullptr;
         if (kt && encode_input_map(kt, x, in_dtype, N0, N1, ld_x, &tmap, &P)) k1 = kt;
         else encode_input_map(k1, x, in_dtype, N0, N1, ld_x, &tmap, &P);  // fills sample_bytes
         int occ = 0;

@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 
 FP32_TOL = 1e-4  # BASELINE.json north_star, complex64 mode
 FP64_TOL = 1e-10  # BASELINE.json north_star, fp64 mode (we require bitwise anyway)
-KERNELS = ("stream", "window")
+KERNELS = ("stream", "window", "stream_tma")
 
 
 def rel_err(got, ref):
