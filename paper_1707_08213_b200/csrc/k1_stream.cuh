@@ -353,8 +353,12 @@ const K1Info *k1_info() {
 // TP1 window columns per CTA so that a CTA is ~128 threads.  Measured on B200
 // with scripts/tune (profiles/TUNING_r01.md): e.g. c4 (16x16) Q=2/TP1=2 831
 // Gcoef/s vs 760 for Q=1/TP1=8; c3 (32x8) Q=3/TP1=2 783; c5 (64x64) Q=3/TP1=1 797.
-constexpr int k1_choose_q(int M0, int M1) {
+// fp64-exact (DBL) butterflies cost ~2x and run without FMA, so the chain that
+// rebuilds the level-Q node (2^Q - 1 butterflies per row) is capped at Q = 2 for
+// m0 = 5 (c3 in fp64: 369 Gcoef/s at Q=2 vs 243 at Q=3, profiles/TUNING_r01.md).
+constexpr int k1_choose_q(int M0, int M1, bool DBL = false) {
     int q = M0 > 2 ? M0 - 2 : 0;
+    if (DBL && M0 == 5) q = 2;
     while (q > 0 && (1 << M1) * (1 << q) > 512) --q;
     return q;
 }
@@ -365,7 +369,7 @@ constexpr int k1_choose_tp1(int M1, int Q) {
 
 template <int M0, int M1, bool DBL> struct K1Inst {
     using T = typename std::conditional<DBL, double, float>::type;
-    static constexpr int Q = k1_choose_q(M0, M1);
+    static constexpr int Q = k1_choose_q(M0, M1, DBL);
     static constexpr int TP1 = k1_choose_tp1(M1, Q);
     using S = K1Shape<M0, M1, Q, TP1>;
     static void reg() {

@@ -18,14 +18,12 @@ struct Variant { const char *name; const K1Info *(*info)(); };
 #define V(T, M0, M1, Q, TP1, MINB, NBM)                                                   \
     {#T " m0=" #M0 " m1=" #M1 " Q=" #Q " TP1=" #TP1 " MINB=" #MINB " NBM=" #NBM,          \
      &k1_info<T, M0, M1, Q, TP1, false, MINB, NBM>}
+#define V64(M0, M1, Q, TP1, MINB)                                                       \
+    {"double m0=" #M0 " m1=" #M1 " Q=" #Q " TP1=" #TP1 " MINB=" #MINB,                  \
+     &k1_info<double, M0, M1, Q, TP1, true, MINB, 1>}
 static const Variant VARIANTS[] = {
-    V(float, 4, 4, 2, 2, 1, 1), V(float, 4, 4, 2, 1, 1, 1), V(float, 4, 4, 2, 2, 6, 1), V(float, 4, 4, 2, 2, 8, 1),
-    V(float, 4, 4, 2, 2, 1, 2), V(float, 4, 4, 2, 2, 1, 4), V(float, 4, 4, 2, 4, 1, 2), V(float, 4, 4, 1, 4, 1, 1),
-    V(float, 4, 4, 3, 1, 1, 1), V(float, 4, 4, 1, 2, 1, 1),
-    V(float, 5, 3, 3, 2, 1, 1), V(float, 5, 3, 3, 1, 1, 1), V(float, 5, 3, 3, 2, 6, 1), V(float, 5, 3, 3, 2, 1, 2),
-    V(float, 5, 3, 2, 4, 1, 1), V(float, 5, 3, 2, 2, 1, 1),
-    V(float, 6, 6, 3, 1, 1, 1), V(float, 6, 6, 4, 1, 1, 1), V(float, 6, 6, 2, 1, 1, 1), V(float, 6, 6, 3, 1, 1, 2),
-    V(float, 6, 6, 2, 1, 2, 1),
+    V64(4, 4, 2, 2, 1), V64(4, 4, 1, 4, 1), V64(4, 4, 1, 2, 1), V64(4, 4, 0, 4, 1), V64(4, 4, 1, 8, 1),
+    V64(5, 3, 3, 2, 1), V64(5, 3, 2, 4, 1), V64(5, 3, 2, 2, 1), V64(5, 3, 1, 4, 1), V64(5, 3, 2, 8, 1),
 };
 }  // namespace swdft2d
 

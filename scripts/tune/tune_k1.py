@@ -33,6 +33,7 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--only", default="")
     ap.add_argument("--configs", default="c2,c3,c4,c5")
+    ap.add_argument("--prec", type=int, default=0, help="0 fp32 / 1 fp64 variants")
     a = ap.parse_args()
     lib = ctypes.CDLL(os.path.join(HERE, "_build", "libtune.so"))
     lib.tune_name.restype = ctypes.c_char_p
@@ -58,11 +59,12 @@ def run_variant(lib, v, name, cfg, cache, dev, flush, a):
             cache.clear()
             torch.cuda.empty_cache()
             x = torch.from_numpy(cfg.generate()).to(dev)
-            out = torch.empty((cfg.P0, cfg.P1, cfg.n0, cfg.n1), dtype=torch.complex64, device=dev)
+            odt = torch.complex128 if a.prec else torch.complex64
+            out = torch.empty((cfg.P0, cfg.P1, cfg.n0, cfg.n1), dtype=odt, device=dev)
             # reference output of the product library: full if it fits, else the first rows
             rows = cfg.P0 if cfg.coefficients * 8 < 60e9 else 64
-            ref = torch.empty((rows, cfg.P1, cfg.n0, cfg.n1), dtype=torch.complex64, device=dev)
-            forward_into(x, m0, m1, ref, prec=_lib.PREC_FP32, p0_end=rows)
+            ref = torch.empty((rows, cfg.P1, cfg.n0, cfg.n1), dtype=odt, device=dev)
+            forward_into(x, m0, m1, ref, prec=a.prec, p0_end=rows)
             cache[cfg.name] = (x, ref, out)
             del x, ref, out
         x, ref, out = cache[cfg.name]
@@ -71,7 +73,7 @@ def run_variant(lib, v, name, cfg, cache, dev, flush, a):
 
         def launch():
             rc = lib.swdft2d_forward(x.data_ptr(), _lib.IN_F32 if x.dtype == torch.float32 else _lib.IN_C64,
-                                     cfg.N0, cfg.N1, cfg.N1, m0, m1, 0, 1.0, 0, cfg.P0,
+                                     cfg.N0, cfg.N1, cfg.N1, m0, m1, a.prec, 1.0, 0, cfg.P0,
                                      out.data_ptr(), 1, s.cuda_stream)
             assert rc == 0, lib.swdft2d_last_error()
 
@@ -95,7 +97,7 @@ def run_variant(lib, v, name, cfg, cache, dev, flush, a):
             err = max(err, float((d / nrm).max()))
         print(json.dumps({"variant": name, "config": cfg.name, "ms": t * 1e3,
                           "gcoef_s": cfg.coefficients / t / 1e9,
-                          "write_gbs": cfg.coefficients * 8 / t / 1e9,
+                          "write_gbs": cfg.coefficients * (16 if a.prec else 8) / t / 1e9,
                           "threads": lib.tune_m(v, 2), "smem": lib.tune_m(v, 3),
                           "max_rel_vs_product": err}), flush=True)
 
