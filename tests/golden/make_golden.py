@@ -192,6 +192,12 @@ def main():
                 rc = ref_cli.main(["verify", "--input", csvp, "--window", "4x2"] + flag)
             res["corrupt" if flag else "plain"] = {"rc": rc, "line": buf.getvalue().strip()}
         nxt["verify"] = res
+        # cmd_transform: CSV in, SWDF out (file bytes)
+        outp = os.path.join(td, "t.swdf")
+        with contextlib.redirect_stdout(_io.StringIO()):
+            rc = ref_cli.main(["transform", "--input", csvp, "--output", outp, "--window", "4x2",
+                               "--normalization", "paper-2d"])
+        nxt["transform"] = {"rc": rc, "sha": hashlib.sha256(open(outp, "rb").read()).hexdigest()}
     sigs = []
     for i, (N, m) in enumerate([(40, 3), (17, 4), (9, 0), (64, 6)]):
         s1 = np.random.default_rng(300 + i).standard_normal(N) + 1j * np.random.default_rng(400 + i).standard_normal(N)

@@ -166,3 +166,17 @@ def test_bench_csv_fig4(cuda, golden):
     for r in recs:
         assert r.ops == meta["next"]["fig4_predict_ops"][str(r.window[0])][r.algorithm]
         assert r.seconds > 0
+
+
+@pytest.mark.gpu
+def test_transform_file_bytes(golden, cuda, tmp_path):
+    """cmd_transform equivalent: CSV -> GPU tree (fp64) -> SWDF, byte-identical to the reference's."""
+    from paper_1707_08213_b200.container import transform_file
+
+    meta, _ = golden
+    x = np.random.default_rng(21).standard_normal((12, 9))
+    csvp = tmp_path / "x.csv"
+    np.savetxt(csvp, x, delimiter=",")
+    shape = transform_file(csvp, tmp_path / "t.swdf", (4, 2), normalization="paper-2d")
+    assert shape == (9, 8, 4, 2)
+    assert file_sha(tmp_path / "t.swdf") == meta["next"]["transform"]["sha"]
