@@ -50,6 +50,7 @@ class SlidingRowStream2D:
                                  device=self.device)
         self.P1 = self.N1 - self.n1 + 1
         self._levels = self._level_plan()
+        self._profiles = self._push_profiles()
         self.rows_pushed = 0
         self.ops_last_push = 0
         self.last_push_position_ops = np.zeros(self.N1, dtype=np.int64)
@@ -64,6 +65,57 @@ class SlidingRowStream2D:
             plan.append((0, 1 << (self.m0 - q), (1 << q) * self.n1))
         return plan
 
+    def _push_profiles(self):
+        """(ops, per-position ops) of a push that runs the row levels and the first c
+        column levels, c = 0..m0 (the per-push arithmetic of tree2d.py:251-293)."""
+        n1, N1 = self.n1, self.N1
+        vec = np.zeros(N1, dtype=np.int64)
+        ops = 0
+        out = []
+        for dim, s, nodes in self._levels:
+            if dim == 1:
+                ops += (N1 - (n1 - s)) * nodes
+                vec[n1 - s:] += nodes
+        out.append((ops, vec.copy()))
+        for dim, s, nodes in self._levels:
+            if dim == 0:
+                ops += (N1 - n1 + 1) * nodes
+                vec[n1 - 1:] += nodes
+                out.append((ops, vec.copy()))
+        return out
+
+    def _col_levels_run(self, p0: int) -> int:
+        """Column levels a push of row p0 runs: those with p0 >= n0 - s (tree2d.py:273-274)."""
+        c = 0
+        for dim, s, _ in self._levels:
+            if dim == 0:
+                if p0 < self.n0 - s:
+                    break
+                c += 1
+        return c
+
+    def _account(self, p0: int, last: bool = True) -> None:
+        """Operation accounting of pushing row p0 (tree2d.py:251-293): the counter's
+        add_region calls level by level, and ops_last_push / last_push_position_ops."""
+        n0, n1, N1 = self.n0, self.n1, self.N1
+        if self.counter is not None:
+            for dim, s, nodes in self._levels:
+                if dim == 1:
+                    self.counter.add_region((p0, slice(n1 - s, N1)), nodes, N1 - (n1 - s))
+                else:
+                    if p0 < n0 - s:
+                        break  # deeper column levels need even more rows
+                    self.counter.add_region((p0, slice(n1 - 1, N1)), nodes, N1 - n1 + 1)
+        if last:
+            ops, vec = self._profiles[self._col_levels_run(p0)]
+            self.ops_last_push = ops
+            np.copyto(self.last_push_position_ops, vec)
+
+    def _store(self, p0: int, r: torch.Tensor) -> None:
+        slot = p0 % self.n0
+        self._ring[slot].copy_(r)
+        self._ring[slot + self.n0].copy_(r)
+
     def push_row(self, row):
         """Ingest one length-N1 row; returns the (P1, n0, n1) slab (device tensor)
         once n0 rows have arrived, None while warming up."""
@@ -76,29 +128,9 @@ class SlidingRowStream2D:
         if tuple(r.shape) != (self.N1,):
             raise core.ShapeError(f"row shape {tuple(r.shape)} != ({self.N1},)")
         p0 = self.rows_pushed
-        slot = p0 % self.n0
-        r = r.to(device=self.device, dtype=self._ring.dtype)
-        self._ring[slot].copy_(r)
-        self._ring[slot + self.n0].copy_(r)
-        # operation accounting, tree2d.py:251-293
-        self.last_push_position_ops[:] = 0
-        ops = 0
-        n0, n1, N1 = self.n0, self.n1, self.N1
-        for dim, s, nodes in self._levels:
-            if dim == 1:
-                lo = n1 - s
-                ops += (N1 - lo) * nodes
-                self.last_push_position_ops[lo:] += nodes
-                if self.counter is not None:
-                    self.counter.add_region((p0, slice(lo, N1)), nodes, N1 - lo)
-            else:
-                if p0 < n0 - s:
-                    break  # deeper column levels need even more rows
-                ops += (N1 - n1 + 1) * nodes
-                self.last_push_position_ops[n1 - 1:] += nodes
-                if self.counter is not None:
-                    self.counter.add_region((p0, slice(n1 - 1, N1)), nodes, N1 - n1 + 1)
-        self.ops_last_push = ops
+        n0, n1 = self.n0, self.n1
+        self._store(p0, r.to(device=self.device, dtype=self._ring.dtype))
+        self._account(p0)
         self.rows_pushed += 1
         if p0 < n0 - 1:
             return None
@@ -108,6 +140,44 @@ class SlidingRowStream2D:
         forward_into(window_rows, self.m0, self.m1, slab, prec=self.prec, scale=self._factor,
                      kernel=self.kernel)
         return slab[0]
+
+    def push_rows(self, rows):
+        """Ingest k rows at once (a [k, N1] block); returns the [k', P1, n0, n1] slabs
+        of every window row completed by the block (k' <= k; None if none).  Equal to
+        k push_row calls (same slabs, same accounting and counter calls), but one K1
+        launch over the block plus the n0 - 1 rows before it."""
+        if self.closed:
+            raise core.StateError("push after close")
+        blk = rows if isinstance(rows, torch.Tensor) else torch.from_numpy(
+            np.asarray(rows, dtype=np.complex128))
+        if blk.dim() != 2 or blk.shape[1] != self.N1:
+            raise core.ShapeError(f"row block shape {tuple(blk.shape)} != (k, {self.N1})")
+        k = int(blk.shape[0])
+        if k == 0:
+            return None
+        n0 = self.n0
+        blk = blk.to(device=self.device, dtype=self._ring.dtype)
+        first = self.rows_pushed
+        pre = min(first, n0 - 1)  # earlier rows the block's first windows need
+        start = (first - pre) % n0
+        work = torch.cat([self._ring[start:start + pre], blk]) if pre else blk.contiguous()
+        if self.counter is not None:
+            for i in range(k - 1):
+                self._account(first + i, last=False)
+        self._account(first + k - 1)
+        for i in range(max(0, k - n0), k):  # keep the last n0 rows for later pushes
+            self._store(first + i, blk[i])
+        self.rows_pushed += k
+        w_begin = max(0, first - n0 + 1)  # global window rows completed by this block
+        w_end = first + k - n0 + 1
+        if w_end <= w_begin:
+            return None
+        base = first - pre  # global row of work[0]
+        out = torch.empty((w_end - w_begin, self.P1, n0, self.n1), dtype=_OUT_DTYPES[self.prec],
+                          device=self.device)
+        forward_into(work, self.m0, self.m1, out, prec=self.prec, scale=self._factor,
+                     p0_begin=w_begin - base, p0_end=w_end - base, kernel=self.kernel)
+        return out
 
     def close(self) -> None:
         self.closed = True

@@ -116,6 +116,40 @@ def test_row_stream_equals_batch(cuda, oracle_lib, shape, m):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("shape,m", [((40, 21), (2, 2)), ((70, 130), (6, 6)), ((9, 12), (3, 1))])
+def test_row_stream_blocks_equal_batch(cuda, oracle_lib, shape, m):
+    """push_rows(block) == the same rows pushed one by one == the batch rows."""
+    from paper_1707_08213_b200.stream import SlidingRowStream2D
+
+    rng = np.random.default_rng(shape[1] + m[1])
+    x = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+    ref = oracle_lib.tree2d(x, *m)
+    c = OpCounter(shape)
+    st = SlidingRowStream2D(WindowSpec(m), shape[1], counter=c)
+    got, r = [], 0
+    for k in [1, 2, 5, 1, (1 << m[0]) + 3, 7, 100]:
+        blk = x[r:r + k]
+        r += len(blk)
+        if len(blk) == 0:
+            break
+        out = st.push_rows(blk)
+        if out is not None:
+            got.append(out.cpu().numpy())
+    got = np.concatenate(got)
+    assert np.array_equal(got.view(np.uint64), ref.view(np.uint64))
+    from paper_1707_08213_b200.tree2d import replay_counter
+
+    cb = OpCounter(shape)
+    replay_counter(cb, shape, WindowSpec(m))
+    assert c.total == cb.total and np.array_equal(c.position_ops, cb.position_ops)
+    st2 = SlidingRowStream2D(WindowSpec(m), shape[1])  # mixed single pushes after a block
+    st2.push_rows(x[:3])
+    tail = [st2.push_row(x[i]) for i in range(3, shape[0])]
+    n0 = 1 << m[0]
+    assert np.array_equal(tail[-1].cpu().numpy().view(np.uint64), ref[-1].view(np.uint64))
+
+
+@pytest.mark.gpu
 def test_row_stream_1x1_matches_reference_stream(golden, cuda):
     from paper_1707_08213_b200.stream import SlidingRowStream2D
 
