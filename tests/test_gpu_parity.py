@@ -238,3 +238,23 @@ def test_linearity_and_transpose(cuda):
     assert np.abs(lhs - rhs).max() <= 1e-10 * max(1, np.abs(rhs).max())
     xt = run(np.ascontiguousarray(x.T), 2, 3, "fp64")
     assert np.abs(xt - run(x, 3, 2, "fp64").transpose(1, 0, 3, 2)).max() <= 1e-10
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+def test_strip_partition_on_device(cuda, world):
+    """Each rank's strip (window rows + n0-1 halo rows, swdft2d_strip_range) computed
+    alone on the device reproduces its rows of the full output bitwise (fp64)."""
+    from paper_1707_08213_b200.partition import strip_plan
+
+    rng = np.random.default_rng(world)
+    x = rng.standard_normal((75, 41))
+    m0, m1 = 3, 2
+    xt = torch.from_numpy(x).to(cuda)
+    P0, P1 = 75 - 7, 41 - 3
+    full = torch.empty((P0, P1, 8, 4), dtype=torch.complex128, device=cuda)
+    forward_into(xt, m0, m1, full, prec=_lib.PREC_FP64)
+    for (a, b, rb, re) in strip_plan(P0, m0, world):
+        part = torch.empty((b - a, P1, 8, 4), dtype=torch.complex128, device=cuda)
+        if b > a:
+            forward_into(xt[rb:re].clone(), m0, m1, part, prec=_lib.PREC_FP64)
+        assert torch.equal(part.view(torch.float64), full[a:b].view(torch.float64))
