@@ -200,7 +200,7 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     from paper_1707_08213_b200 import WindowSpec, tree_swdft_2d
     from paper_1707_08213_b200 import _lib
-    from paper_1707_08213_b200.partition import scatter_strips, strip_plan
+    from paper_1707_08213_b200.partition import pipelined_strip_forward, strip_plan
     from paper_1707_08213_b200.tree2d import _OUT_DTYPES, _precision_code, forward_into
 
     torch.cuda.set_device(local_rank)
@@ -222,15 +222,18 @@ def run_ours(args, cfg, rank, world, local_rank):
         x_full = torch.from_numpy(x_np).to(dev)
     recv = None if rank == 0 else torch.empty((re - rb, cfg.N1), dtype=xdt, device=dev)
 
+    def compute(local, w0, w1):
+        forward_into(local, cfg.m0, cfg.m1, out[w0:w1], prec=prec, p0_begin=w0, p0_end=w1,
+                     stream=stream)
+
     def step():
-        # N > 1: the partitioner's scatter (one batched NCCL group of sends from rank 0)
+        # N > 1: the partitioner's pipelined scatter — every strip travels from rank 0 in
+        # two in-order chunks and each rank starts on its first (1/8) chunk on arrival
         if world > 1:
-            src, _ = scatter_strips(x_full if rank == 0 else None, (cfg.N0, cfg.N1), cfg.m0, xdt,
-                                    dev, recv=recv)
-        else:
-            src = x_full
-        if b > a:
-            forward_into(src, cfg.m0, cfg.m1, out, prec=prec, stream=stream)
+            pipelined_strip_forward(x_full if rank == 0 else None, (cfg.N0, cfg.N1), cfg.m0, xdt,
+                                    dev, compute, recv=recv)
+        elif b > a:
+            compute(x_full, 0, b - a)
 
     if world > 1:
         dist.barrier()

@@ -89,8 +89,72 @@ def scatter_strips(x, shape, m0: int, dtype, device, group=None, src: int = 0, r
     return local, my
 
 
+def piece_bounds(rows: int, first_fraction: float, pieces: int):
+    """Window-row pieces [w_c, w_{c+1}) of a strip: a short first piece (so compute
+    starts after a small part of the strip has arrived), the rest split evenly."""
+    if rows <= 0:
+        return [0, 0]
+    if pieces <= 1 or rows < 2:
+        return [0, rows]
+    first = max(1, min(rows - 1, int(round(rows * first_fraction))))
+    rest = pieces - 1
+    bounds = [0, first]
+    for c in range(1, rest + 1):
+        bounds.append(first + ((rows - first) * c) // rest)
+    return sorted(set(bounds))
+
+
+def pipelined_strip_forward(x, shape, m0: int, dtype, device, compute, group=None, src: int = 0,
+                            recv=None, pieces: int = 2, first_fraction: float = 0.125):
+    """Scatter + compute with overlap: every rank's strip travels as ``pieces``
+    consecutive row chunks (separate point-to-point messages, in order), and
+    ``compute(local_rows, w_begin, w_end)`` runs for window rows [w_begin, w_end)
+    (strip-relative) as soon as the input rows they need, [w_begin, w_end + n0 - 1),
+    have arrived — so rank g starts after its first (short) chunk instead of after
+    its whole strip.  The source rank computes its own strip at once.
+    Returns (local_rows_tensor, (p0_begin, p0_end, row_begin, row_end)).
+    """
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    N0, N1 = int(shape[0]), int(shape[1])
+    n0 = 1 << m0
+    P0 = N0 - n0 + 1
+    plan = strip_plan(P0, m0, world)
+    a, b, rb, re = plan[rank]
+    if rank == src:
+        if x is None or tuple(x.shape) != (N0, N1):
+            raise core.ShapeError(f"source rank needs the full {N0}x{N1} input")
+        works = []
+        for g, (ga, gb, grb, gre) in enumerate(plan):
+            if g == src or gre <= grb:
+                continue
+            wb = piece_bounds(gb - ga, first_fraction, pieces)
+            cuts = [0] + [w + n0 - 1 for w in wb[1:-1]] + [gre - grb]
+            for c in range(len(cuts) - 1):  # in order: the peer computes piece c on arrival
+                works.append(dist.isend(x[grb + cuts[c]:grb + cuts[c + 1]].contiguous(), g,
+                                        group=group))
+        local = x[rb:re]
+        if b > a:
+            compute(local, 0, b - a)
+        for w in works:
+            w.wait()
+        return local, (a, b, rb, re)
+    local = recv if recv is not None else torch.empty((re - rb, N1), dtype=dtype, device=device)
+    if tuple(local.shape) != (re - rb, N1):
+        raise ValueError(f"recv buffer must have shape {(re - rb, N1)}")
+    if b > a:
+        wb = piece_bounds(b - a, first_fraction, pieces)
+        cuts = [0] + [w + n0 - 1 for w in wb[1:-1]] + [re - rb]
+        works = [dist.irecv(local[cuts[c]:cuts[c + 1]], src, group=group)
+                 for c in range(len(cuts) - 1)]
+        for c in range(len(wb) - 1):
+            works[c].wait()  # NCCL: the compute stream waits for this chunk only
+            compute(local, wb[c], wb[c + 1])
+    return local, (a, b, rb, re)
+
+
 def tree_swdft_2d_sharded(x, spec, *, shape=None, dtype=None, group=None, src: int = 0,
-                          precision=None, budget=None) -> ShardedCoefficients:
+                          precision=None, budget=None, pieces: int = 2) -> ShardedCoefficients:
     """Strip-sharded tree_swdft_2d: every rank returns its own window rows.
 
     On ``src`` pass the full input tensor (CUDA); elsewhere pass x=None plus
@@ -109,15 +173,19 @@ def tree_swdft_2d_sharded(x, spec, *, shape=None, dtype=None, group=None, src: i
         raise core.ShapeError("tree_swdft_2d expects a 2D array and 2D window")
     spec.check_fits(shape)
     m0, m1 = (int(m) for m in spec.exponents)
-    local, (a, b, rb, re) = scatter_strips(x, shape, m0, dtype, device, group, src)
     prec = _precision_code(precision, dtype)
     n0, n1 = 1 << m0, 1 << m1
-    P1 = shape[1] - n1 + 1
+    P0, P1 = shape[0] - n0 + 1, shape[1] - n1 + 1
+    a, b, rb, re = strip_plan(P0, m0, dist.get_world_size(group))[dist.get_rank(group)]
     if b > a:
         sshape = (re - rb, shape[1])
         core.check_budget(core.lattice_bytes(sshape, spec) + core.output_bytes(sshape, spec),
                           budget, what="level buffers + coefficient output")
     out = torch.empty((b - a, P1, n0, n1), dtype=_OUT_DTYPES[prec], device=device)
-    if b > a:
-        forward_into(local, m0, m1, out, prec=prec, scale=core.normalization_factor(spec))
+    scale = core.normalization_factor(spec)
+
+    def compute(local, w0, w1):
+        forward_into(local, m0, m1, out[w0:w1], prec=prec, scale=scale, p0_begin=w0, p0_end=w1)
+
+    pipelined_strip_forward(x, shape, m0, dtype, device, compute, group, src, pieces=pieces)
     return ShardedCoefficients(out, a, b, tuple(shape), spec, spec.normalization)

@@ -43,10 +43,32 @@ for G in (1, 2, 4, 8):
             ts.append(e0.elapsed_time(e1) / 1e3)
         times.append(min(ts))
     tmax = max(times)
+    # the pipelined receive splits each strip into a 1/8 piece and the rest (two launches)
+    from paper_1707_08213_b200.partition import piece_bounds
+
+    a, b, rb, re = max(plan, key=lambda p: p[1] - p[0])
+    wb = piece_bounds(b - a, 0.125, 2)
+    ts = []
+    for _ in range(3):
+        flush.fill_(1.0)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for c in range(len(wb) - 1):
+            forward_into(x[rb:re], cfg.m0, cfg.m1, out[wb[c]:wb[c + 1]], prec=prec,
+                         p0_begin=wb[c], p0_end=wb[c + 1])
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) / 1e3)
+    t_piece1 = None
     t1 = t1 or tmax
     scatter_bytes = sum((re - rb) * cfg.N1 * x.element_size() for g, (a, b, rb, re) in enumerate(plan) if g)
     t_scatter = scatter_bytes / (PEER_GBS * 1e9)
+    t_two = min(ts)
+    first_bytes = (wb[1] + cfg.n0 - 1) * cfg.N1 * x.element_size() * (G - 1)  # all peers' first chunks
+    t_first = first_bytes / (PEER_GBS * 1e9) if G > 1 else 0.0
     res.append({"config": cfg.name, "G": G, "strip_kernel_ms_max": tmax * 1e3,
+                "two_piece_ms": t_two * 1e3, "first_chunks_ms_at_770GBps": t_first * 1e3,
+                "efficiency_pipelined": t1 / (G * (t_two + t_first)) if G > 1 else 1.0,
                 "strip_kernel_ms_min": min(times) * 1e3,
                 "compute_efficiency": t1 / (G * tmax),
                 "scatter_bytes": scatter_bytes, "scatter_ms_at_770GBps": t_scatter * 1e3,

@@ -258,3 +258,28 @@ def test_strip_partition_on_device(cuda, world):
         if b > a:
             forward_into(xt[rb:re].clone(), m0, m1, part, prec=_lib.PREC_FP64)
         assert torch.equal(part.view(torch.float64), full[a:b].view(torch.float64))
+
+
+def test_sharded_api_world1(cuda):
+    """tree_swdft_2d_sharded through a real NCCL process group of size 1 equals tree_swdft_2d."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_1707_08213_b200.partition import tree_swdft_2d_sharded
+
+    with socket.socket() as sck:
+        sck.bind(("127.0.0.1", 0))
+        port = sck.getsockname()[1]
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=cuda)
+    try:
+        x = torch.from_numpy(np.random.default_rng(8).standard_normal((60, 50))).to(cuda)
+        sh = tree_swdft_2d_sharded(x, WindowSpec((3, 2), "unitary"), precision="fp64")
+        ref = tree_swdft_2d(x, WindowSpec((3, 2), "unitary"), precision="fp64").values
+        assert (sh.p0_begin, sh.p0_end) == (0, 53)
+        assert torch.equal(sh.values.view(torch.float64), ref.view(torch.float64))
+    finally:
+        dist.destroy_process_group()
