@@ -200,7 +200,7 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     from paper_1707_08213_b200 import WindowSpec, tree_swdft_2d
     from paper_1707_08213_b200 import _lib
-    from paper_1707_08213_b200.partition import pipelined_strip_forward, strip_plan
+    from paper_1707_08213_b200.partition import choose_pieces, pipelined_strip_forward, strip_plan
     from paper_1707_08213_b200.tree2d import _OUT_DTYPES, _precision_code, forward_into
 
     torch.cuda.set_device(local_rank)
@@ -222,6 +222,9 @@ def run_ours(args, cfg, rank, world, local_rank):
         x_full = torch.from_numpy(x_np).to(dev)
     recv = None if rank == 0 else torch.empty((re - rb, cfg.N1), dtype=xdt, device=dev)
 
+    pieces = choose_pieces((cfg.N0, cfg.N1), cfg.m0, cfg.m1, np.dtype(cfg.dtype).itemsize,
+                           out.element_size(), world)
+
     def compute(local, w0, w1):
         forward_into(local, cfg.m0, cfg.m1, out[w0:w1], prec=prec, p0_begin=w0, p0_end=w1,
                      stream=stream)
@@ -231,7 +234,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         # two in-order chunks and each rank starts on its first (1/8) chunk on arrival
         if world > 1:
             pipelined_strip_forward(x_full if rank == 0 else None, (cfg.N0, cfg.N1), cfg.m0, xdt,
-                                    dev, compute, recv=recv)
+                                    dev, compute, recv=recv, pieces=pieces)
         elif b > a:
             compute(x_full, 0, b - a)
 
@@ -301,7 +304,8 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "output_bytes": cfg.coefficients * out_bpc,
                    "l2": "256 MiB flush write between timed steps (outside the events); "
                          "output >> L2 as well",
-                   "parallelism": f"strips{world}" if world > 1 else "single"},
+                   "parallelism": f"strips{world}" if world > 1 else "single",
+                   "scatter_pieces": pieces},
         "hbm_write_gbs": cfg.coefficients * out_bpc / step_s / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": ncu_traffic(cfg.name),

@@ -104,6 +104,28 @@ def piece_bounds(rows: int, first_fraction: float, pieces: int):
     return sorted(set(bounds))
 
 
+NVLINK_PEER_BPS = 770e9  # measured peer-copy rate per direction (B200_PROFILING.md)
+HBM_WRITE_BPS = 6.4e12   # K1's sustained coefficient write rate on one B200 (profiles/)
+
+
+def choose_pieces(shape, m0: int, m1: int, in_bytes: int, out_bytes: int, world: int) -> int:
+    """2 (pipelined: compute on a 1/8 first chunk while the rest arrives) when the scatter
+    time it hides exceeds the extra launch's n0 - 1 halo rows of compute, else 1.
+    Model: a window row costs P1*n0*n1*out_bytes / HBM_WRITE_BPS; rank 0's egress
+    carries every other strip at NVLINK_PEER_BPS (single-GPU emulation in
+    profiles/strip_scaling_r01.jsonl)."""
+    if world <= 1:
+        return 1
+    N0, N1 = shape
+    n0, n1 = 1 << m0, 1 << m1
+    P0, P1 = N0 - n0 + 1, N1 - n1 + 1
+    row_t = P1 * n0 * n1 * out_bytes / HBM_WRITE_BPS
+    strip_rows = P0 / world
+    send_all = (world - 1) * (strip_rows + n0 - 1) * N1 * in_bytes / NVLINK_PEER_BPS
+    send_first = (world - 1) * (strip_rows / 8 + n0 - 1) * N1 * in_bytes / NVLINK_PEER_BPS
+    return 2 if send_all - send_first > (n0 - 1) * row_t + 5e-6 else 1
+
+
 def pipelined_strip_forward(x, shape, m0: int, dtype, device, compute, group=None, src: int = 0,
                             recv=None, pieces: int = 2, first_fraction: float = 0.125):
     """Scatter + compute with overlap: every rank's strip travels as ``pieces``
@@ -154,7 +176,7 @@ def pipelined_strip_forward(x, shape, m0: int, dtype, device, compute, group=Non
 
 
 def tree_swdft_2d_sharded(x, spec, *, shape=None, dtype=None, group=None, src: int = 0,
-                          precision=None, budget=None, pieces: int = 2) -> ShardedCoefficients:
+                          precision=None, budget=None, pieces=None) -> ShardedCoefficients:
     """Strip-sharded tree_swdft_2d: every rank returns its own window rows.
 
     On ``src`` pass the full input tensor (CUDA); elsewhere pass x=None plus
@@ -183,6 +205,9 @@ def tree_swdft_2d_sharded(x, spec, *, shape=None, dtype=None, group=None, src: i
                           budget, what="level buffers + coefficient output")
     out = torch.empty((b - a, P1, n0, n1), dtype=_OUT_DTYPES[prec], device=device)
     scale = core.normalization_factor(spec)
+    if pieces is None:
+        pieces = choose_pieces(shape, m0, m1, torch.empty((), dtype=dtype).element_size(),
+                               out.element_size(), dist.get_world_size(group))
 
     def compute(local, w0, w1):
         forward_into(local, m0, m1, out[w0:w1], prec=prec, scale=scale, p0_begin=w0, p0_end=w1)
