@@ -214,6 +214,19 @@ def main():
     nxt["fig4_predict_ops"] = {f"{w}": {a: int(ref_bench.predict_ops(a, (100, 100), (w, w)))
                                         for a in ("tree", "fft", "naive")}
                                for w in (4, 8, 16, 32, 64)}
+    # kD (treekd.tree_swdft_kd), SPEC acceptance 6 shapes plus a larger 3D case
+    from swdft import treekd as ref_treekd  # noqa: E402
+    kd = []
+    for i, (shape, m, mode) in enumerate([((6, 6, 6), (1, 1, 1), "none"), ((6, 6, 6), (2, 1, 1), "none"),
+                                          ((4, 4, 4, 4), (1, 1, 1, 1), "none"),
+                                          ((12, 10, 9), (2, 1, 2), "unitary"), ((9, 8, 7), (3, 0, 2), "none")]):
+        rng = np.random.default_rng(600 + i)
+        xk = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+        c = ref_bench.OpCounter(shape)
+        v = ref_treekd.tree_swdft_kd(xk, ref_core.WindowSpec(m, mode), counter=c).values
+        kd.append({"shape": list(shape), "m": list(m), "mode": mode, "seed": 600 + i, "sha": sha(v),
+                   "total": int(c.total), "pos_sha": sha(c.position_ops)})
+    nxt["treekd"] = kd
     meta["next"] = nxt
 
     # --- twiddles

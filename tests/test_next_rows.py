@@ -62,6 +62,17 @@ def test_bench_predict_ops(golden):
             assert predict_ops(alg, (100, 100), (int(w), int(w))) == ops
 
 
+def test_treekd_counter_replay(golden):
+    from paper_1707_08213_b200.treekd import level_regions_kd
+
+    meta, _ = golden
+    for rec in meta["next"]["treekd"]:
+        c = OpCounter(tuple(rec["shape"]))
+        for region, nodes, positions in level_regions_kd(tuple(rec["shape"]), rec["m"]):
+            c.add_region(region, nodes, positions)
+        assert c.total == rec["total"] and sha(c.position_ops) == rec["pos_sha"]
+
+
 # ---------------------------------------------------------------- GPU
 
 @pytest.mark.gpu
@@ -214,3 +225,33 @@ def test_transform_file_bytes(golden, cuda, tmp_path):
     shape = transform_file(csvp, tmp_path / "t.swdf", (4, 2), normalization="paper-2d")
     assert shape == (9, 8, 4, 2)
     assert file_sha(tmp_path / "t.swdf") == meta["next"]["transform"]["sha"]
+
+
+@pytest.mark.gpu
+def test_treekd_bitwise(golden, cuda):
+    """k-D tree by composition (slices through K1, then a dim-0 K1 pass): bitwise equal to the
+    reference's generic engine, counter calls equal (SPEC acceptance 6 shapes)."""
+    from paper_1707_08213_b200.treekd import tree_swdft_kd
+
+    meta, _ = golden
+    for rec in meta["next"]["treekd"]:
+        rng = np.random.default_rng(rec["seed"])
+        shape = tuple(rec["shape"])
+        x = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+        c = OpCounter(shape)
+        v = tree_swdft_kd(x, WindowSpec(tuple(rec["m"]), rec["mode"]), counter=c).values
+        assert sha(v.cpu().numpy()) == rec["sha"], rec
+        assert c.total == rec["total"] and sha(c.position_ops) == rec["pos_sha"]
+    # 2D through the kD entry equals the 2D drop-in
+    from paper_1707_08213_b200 import tree_swdft_2d
+
+    x2 = np.random.default_rng(3).standard_normal((20, 17))
+    a = tree_swdft_kd(x2, WindowSpec((2, 3))).values
+    b = tree_swdft_2d(x2, WindowSpec((2, 3))).values
+    assert torch_equal(a, b)
+
+
+def torch_equal(a, b):
+    import torch
+
+    return torch.equal(a, b)
