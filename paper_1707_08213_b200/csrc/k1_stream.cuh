@@ -56,8 +56,8 @@ template <int N, typename F> __device__ __forceinline__ void static_for(F &&f) {
     static_for_impl(f, std::make_integer_sequence<int, N>{});
 }
 
-constexpr int cmax(int a, int b) { return a > b ? a : b; }
-constexpr int cmin(int a, int b) { return a < b ? a : b; }
+__host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
+__host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
 constexpr int pow2ceil(int v) {
     int p = 1;
     while (p < v) p <<= 1;
@@ -94,7 +94,7 @@ template <typename T, int M0, int M1, int Q, int TP1, int NBM = 1, bool TMA = fa
 constexpr size_t k1_smem_bytes() {
     using S = K1Shape<M0, M1, Q, TP1, NBM>;
     return (TMA ? (size_t)S::STAGE_BYTES : 0) +
-           sizeof(cplx<T>) * ((size_t)S::D * TP1 * S::n1 + S::NMAX);
+           sizeof(cplx<T>) * ((size_t)2 * S::D * TP1 * S::n1 + S::NMAX);
 }
 
 template <typename T, int M0, int M1, int Q, int TP1, bool EXACT, int MINB = 1, int NBM = 1,
@@ -109,8 +109,10 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
     unsigned char *stage = smem_raw;  // TMA: 2 x [NB][row] input tiles (128-B aligned)
-    C *ring = reinterpret_cast<C *>(smem_raw + (TMA ? S::STAGE_BYTES : 0));  // [D][TP1][n1]
-    C *tw = ring + D * TP1 * n1;                                             // make_twiddles(NMAX)
+    // Z ring [2D][TP1][n1]: row r is stored at slot r mod D and again at slot + D, so the
+    // J rows stage C reads (r - t*n0/J) sit at constant offsets below slot + D
+    C *ring = reinterpret_cast<C *>(smem_raw + (TMA ? S::STAGE_BYTES : 0));
+    C *tw = ring + 2 * D * TP1 * n1;  // make_twiddles(NMAX)
     __shared__ __align__(8) uint64_t mbar[S::NSTAGE];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -253,7 +255,10 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
                     if (pl < TP1) {
                         C *dst = ring + ((b * NB + rr) & (D - 1)) * (TP1 * n1) + pl * n1 + lam * V;
 #pragma unroll
-                        for (int be = 0; be < V; ++be) dst[be] = s[be];
+                        for (int be = 0; be < V; ++be) {
+                            dst[be] = s[be];
+                            dst[be + D * TP1 * n1] = s[be];
+                        }
                     }
                 }
             }
@@ -263,21 +268,23 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
             }
             // ---------------- stage C: column trees, NB rows, UNR rows per unrolled block
             // (UNR is a multiple of every register-ring depth, so ring slots are static)
+            // this batch's first slot + D: NB divides D, so batch rows never wrap
+            const C *zb = ring + (((b * NB) & (D - 1)) + D) * (TP1 * n1) + pos * n1 + k1;
 #pragma unroll 1
             for (int k0r = 0; k0r < NB; k0r += S::UNR) {
+                const C *zr = zb + k0r * (TP1 * n1);
                 static_for<S::UNR>([&](auto kuc) {
                     constexpr int ku = decltype(kuc)::value;
                     const int rel = b * NB + k0r + ku;
                     C v[J];
                     static_for<J>([&](auto tc) {
                         constexpr int t = decltype(tc)::value;
-                        v[t] = ring[((rel - t * (n0 / J)) & (D - 1)) * (TP1 * n1) + pos * n1 + k1];
+                        v[t] = zr[(ku - t * (n0 / J)) * (TP1 * n1)];
                     });
                     // levels 1..Q: node j of this row's tree (the reference DAG, tree2d.py:109-112)
                     static_for<Q>([&](auto lc) {
                         constexpr int l = decltype(lc)::value + 1;
-                        constexpr int sl = n0 >> l;
-                        const C w = tw[((j & ((1 << l) - 1)) * sl) * ST0];
+                        const C w = tw[((j & ((1 << l) - 1)) * (n0 >> l)) * ST0];
                         static_for<(1 << (Q - l))>([&](auto tc) {
                             constexpr int t = decltype(tc)::value;
                             v[t] = bfly<EXACT>(v[t + (1 << (Q - l))], w, v[t]);
