@@ -373,6 +373,10 @@ int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t
         const int64_t rows = p0_end - p0_begin;
         const int64_t slots = (int64_t)ds->sms * occ;
         P.RCH = k1_rows_per_tile(rows, P.CB, slots, n0);
+        if (const char *e = std::getenv("SWDFT2D_K1_RCH")) {  // tuning override (rows per tile)
+            const long long v = std::atoll(e);
+            if (v > 0) P.RCH = v < rows ? v : rows;
+        }
         P.ntiles = P.CB * ((rows + P.RCH - 1) / P.RCH);
         double re[K1_TW_N], im[K1_TW_N];
         host_twiddles(K1_TW_N, re, im);

@@ -283,3 +283,19 @@ def test_sharded_api_world1(cuda):
         assert torch.equal(sh.values.view(torch.float64), ref.view(torch.float64))
     finally:
         dist.destroy_process_group()
+
+
+def test_large_windows_k0_and_unsupported(cuda, oracle_lib):
+    """Windows above K1's 2^6 run on K0 (bitwise); above 2^10 the ABI refuses loudly."""
+    from paper_1707_08213_b200 import UnsupportedError
+
+    rng = np.random.default_rng(12)
+    x = rng.standard_normal((140, 12)) + 1j * rng.standard_normal((140, 12))
+    ref = oracle_lib.tree2d(x, 7, 2)
+    assert bits_equal(run(x, 7, 2, "fp64"), ref)                   # auto -> K0 (m0 = 7)
+    assert rel_err(run(x.astype(np.complex64), 7, 2, "fp32"), ref) <= FP32_TOL
+    with pytest.raises(UnsupportedError):
+        run(x, 7, 2, "fp64", kernel="stream")                     # K1 not instantiated
+    y = np.zeros((2048, 2))
+    with pytest.raises(UnsupportedError):
+        run(y, 11, 0, "fp64")                                     # beyond K0's 2^10
