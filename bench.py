@@ -316,9 +316,14 @@ def run_ours(args, cfg, rank, world, local_rank):
         "gpu_launches": args.steps,
     }
 
-    # e2e through the public API from pinned host memory (N=1 only)
-    if world == 1 and not args.no_e2e:
-        line["e2e"] = e2e_host(args, cfg, x_np, dev, spec, odt, out)
+    # e2e through the public API from pinned host memory
+    if not args.no_e2e:
+        if world == 1:
+            line["e2e"] = e2e_host(args, cfg, x_np, dev, spec, odt, out)
+        else:
+            del out
+            torch.cuda.empty_cache()
+            line["e2e"] = e2e_sharded(args, cfg, x_np, dev, spec, xdt, prec, rank, world)
     if world == 1 and not args.no_cpu:
         rate, t, coefs = cpu_reference_rate(cfg, args.ref_rows, 3, host_cores())
         line["cpu_baseline"] = {
@@ -328,6 +333,51 @@ def run_ours(args, cfg, rank, world, local_rank):
                       f"(oracle/swdft2d_oracle.c, complex128) on {cpu_model()}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def e2e_sharded(args, cfg, x_np, dev, spec, xdt, prec, rank, world):
+    """N > 1: rank 0's pinned host input -> H2D -> tree_swdft_2d_sharded (pipelined NCCL
+    scatter + K1 per strip) -> every rank copies its strip of coefficients to its own
+    pinned host buffer (each GPU's own PCIe link).  Time = max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1707_08213_b200.partition import strip_plan, tree_swdft_2d_sharded
+
+    a, b, _, _ = strip_plan(cfg.P0, cfg.m0, world)[rank]
+    x_pin = torch.from_numpy(x_np).pin_memory() if rank == 0 else None
+    from paper_1707_08213_b200.tree2d import _OUT_DTYPES
+
+    host_out = torch.empty((b - a, cfg.P1, cfg.n0, cfg.n1), dtype=_OUT_DTYPES[prec],
+                           pin_memory=True)
+    stream = torch.cuda.current_stream(dev)
+    times = []
+    for i in range(args.warmup + args.e2e_steps):
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        xd = x_pin.to(dev, non_blocking=True) if rank == 0 else None
+        sh = tree_swdft_2d_sharded(xd, spec, shape=(cfg.N0, cfg.N1), dtype=xdt,
+                                   precision="fp32" if prec == 0 else "fp64", budget=1 << 62)
+        host_out.copy_(sh.values, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        del sh, xd
+        if i >= args.warmup:
+            times.append(e0.elapsed_time(e1) / 1e3)
+    t = torch.tensor([statistics.mean(times)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    d2h = torch.tensor([host_out.numel() * host_out.element_size()], dtype=torch.float64,
+                       device=dev)
+    dist.all_reduce(d2h)
+    s = float(t.item())
+    return {"value": cfg.coefficients / s, "unit": UNIT,
+            "h2d_bytes_per_step": int(cfg.in_bytes), "d2h_bytes_per_step": int(d2h.item()),
+            "ms_per_step": s * 1e3, "steps": len(times),
+            "path": "rank 0 pinned host input -> tree_swdft_2d_sharded -> each rank's strip "
+                    "to its own pinned host buffer; max over ranks"}
 
 
 def e2e_host(args, cfg, x_np, dev, spec, odt, out_dev):
