@@ -313,7 +313,8 @@ def run_ours(args, cfg, rank, world, local_rank):
                      "bytes_per_launch": bytes_alg, "kernel_ms": kern_s * 1e3},
         "kernel": dict(_lib.stream_kernel_info(cfg.m0, cfg.m1, prec), name="K1 k1_stream_kernel"),
         "clocks": clk.summary(),
-        "gpu_launches": args.steps,
+        # K1 launches per step: one at N=1; up to `pieces` per rank under the pipelined scatter
+        "gpu_launches": args.steps * (1 if world == 1 else pieces),
     }
 
     # e2e through the public API from pinned host memory
