@@ -39,7 +39,7 @@ METRICS = {
     "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio": "stall_short_sb",
     "smsp__average_warps_issue_stalled_lg_throttle_per_issue_active.ratio": "stall_lg_throttle",
 }
-SCALE = {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3, "nsecond": 1e-9,
+SCALE = {"nsecond": 1e-9, "ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3, "msecond": 1e-3, "nsecond": 1e-9,
          "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
          "byte/second": 1, "Gbyte/second": 1e9, "Tbyte/second": 1e12, "Mbyte/second": 1e6,
          "byte/s": 1, "Mbyte/s": 1e6, "Gbyte/s": 1e9, "Tbyte/s": 1e12,
@@ -63,9 +63,36 @@ def read_raw(rep):
     return res
 
 
+def traffic_table(paths):
+    """Single-pass `ncu --metrics dram__bytes_*` CSVs (TRAFFIC_CSV:CONFIG) of full launches."""
+    rows = ["", "## Full-launch DRAM traffic (single-pass `ncu --metrics "
+            "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum`)", "",
+            "| config | launch | duration ms | alg GB | dram read GB | dram write GB | traffic/alg | "
+            "write TB/s |", "|---|---|---|---|---|---|---|---|"]
+    per_cfg = {}
+    for spec in paths:
+        path, name = spec.split(":")
+        cfg = CONFIGS[name]
+        lines = [l for l in open(path) if not l.startswith("==")]
+        per = {}
+        for row in csv.DictReader(lines):
+            v = float(row["Metric Value"].replace(",", "")) * SCALE.get(row["Metric Unit"], 1.0)
+            per.setdefault(int(row["ID"]), {})[row["Metric Name"]] = v
+        alg = cfg.algorithmic_bytes()
+        for i, (_, m) in enumerate(sorted(per.items())):
+            rd, wr = m["dram__bytes_read.sum"], m["dram__bytes_write.sum"]
+            du = m["gpu__time_duration.sum"]
+            rows.append(f"| {name} | {i} | {du * 1e3:.3f} | {alg / 1e9:.3f} | {rd / 1e9:.4f} | "
+                        f"{wr / 1e9:.3f} | {(rd + wr) / alg:.4f} | "
+                        f"{m['dram__bytes_write.sum.per_second'] / 1e12:.2f} |")
+            per_cfg[name] = {"dram_bytes_per_launch": rd + wr, "full_launch_duration_s": du}
+    return rows, per_cfg
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--round", required=True)
+    ap.add_argument("--traffic", nargs="*", default=[], help="TRAFFIC_CSV:CONFIG")
     ap.add_argument("captures", nargs="+")
     a = ap.parse_args()
     summ_path = os.path.join(ROOT, "profiles", "ncu_summary.json")
@@ -98,6 +125,11 @@ def main():
                       "alg_bytes": alg, "traffic_bytes": traffic, "traffic_over_alg": traffic / alg})
             if rows == cfg.P0:
                 e["dram_bytes_per_launch"] = traffic
+    if a.traffic:
+        trows, per_cfg = traffic_table(a.traffic)
+        lines += trows
+        for name, d in per_cfg.items():
+            summ.setdefault(name, {}).update(d)
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
     with open(os.path.join(ROOT, "profiles", f"ncu_{a.round}.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
