@@ -13,11 +13,16 @@
 //
 // CTA = TP1 consecutive window columns x all n1 frequencies k1 x J "k0
 // residue groups".  Thread (k1, j, pos) owns column (pos, k1) and the output
-// frequencies k0 = j + J*u.  Work is done in batches of NB input rows:
+// frequencies k0 = j + J*u.  A persistent grid walks (column block, row chunk)
+// tiles; each tile is processed in batches of NB input rows:
+//   0. input: the batch's NB x (TP1 + n1 - 1) samples arrive either by per-lane
+//      loads issued one batch ahead into registers (default), or (TMA=true) as a
+//      cp.async.bulk.tensor tile in a 4-stage shared-memory ring with mbarriers.
 //   1. stage R: the warps split the NB x TP1 row transforms; each transform
 //      is an n1-point radix-2 DIT on G = min(n1, 32) lanes (V = n1/G values
 //      per lane) with warp shuffles for the level exchanges, written into a
-//      shared-memory ring Z[D][TP1][n1] (D >= n0 rows of history).
+//      shared-memory ring Z (D >= n0 - n0/J + NB rows; every row stored twice,
+//      at slot and slot + D, so stage C reads at constant offsets).
 //   2. __syncthreads
 //   3. stage C, per row: the thread rebuilds the level-Q node j of its column
 //      tree from J ring rows (2^Q - 1 butterflies, the reference DAG), then
@@ -80,8 +85,8 @@ template <int M0, int M1, int Q, int TP1, int NBM = 1> struct K1Shape {
     static constexpr int RING = cmax((M0 - Q) * (n0 / (2 * J)), 1);  // register ring, complex
     static constexpr int OUTS = n0 / J;                   // coefficients per thread per row
     static constexpr int UNR = cmin(cmax(n0 / (2 * J), 8), NB);  // stage-C rows per unrolled block
-    // TMA staging: 2 stages x NB rows x (TP1 + n1 - 1) samples of <= 16 B, plus up to
-    // 16 B in front (the box starts on a 16-B aligned column), rows 16-B padded
+    // TMA staging: NSTAGE stages x NB rows x (TP1 + n1 - 1) samples of <= 16 B, plus up
+    // to 16 B in front (the box starts on a 16-B aligned column), rows 16-B padded
     static constexpr int STAGE_ROW_MAX = ((TP1 + n1 - 1) * 16 + 15) / 16 * 16 + 16;
     static constexpr int STAGE_SPAN = (NB * STAGE_ROW_MAX + 127) / 128 * 128;  // 128-B aligned
     static constexpr int NSTAGE = 4;  // TMA tiles in flight: batch b loads while b-3 computes
@@ -108,7 +113,7 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
     constexpr int ST0 = NMAX / n0, ST1 = NMAX / n1;  // table strides (exact, App. A #4)
 
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    unsigned char *stage = smem_raw;  // TMA: 2 x [NB][row] input tiles (128-B aligned)
+    unsigned char *stage = smem_raw;  // TMA: NSTAGE x [NB][row] input tiles (128-B aligned)
     // Z ring [2D][TP1][n1]: row r is stored at slot r mod D and again at slot + D, so the
     // J rows stage C reads (r - t*n0/J) sit at constant offsets below slot + D
     C *ring = reinterpret_cast<C *>(smem_raw + (TMA ? S::STAGE_BYTES : 0));
