@@ -325,6 +325,12 @@ def run_ours(args, cfg, rank, world, local_rank):
             del out
             torch.cuda.empty_cache()
             line["e2e"] = e2e_sharded(args, cfg, x_np, dev, spec, xdt, prec, rank, world)
+    if world == 1 and not args.no_others:
+        if graph is not None:
+            del graph
+        del out
+        torch.cuda.empty_cache()
+        line["other_configs"] = other_configs(args, cfg, dev, flush, stream)
     if world == 1 and not args.no_cpu:
         rate, t, coefs = cpu_reference_rate(cfg, args.ref_rows, 3, host_cores())
         line["cpu_baseline"] = {
@@ -334,6 +340,46 @@ def run_ours(args, cfg, rank, world, local_rank):
                       f"(oracle/swdft2d_oracle.c, complex128) on {cpu_model()}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def other_configs(args, main_cfg, dev, flush, stream):
+    """The other BASELINE configs on the same GPU in the same run (kernel-only, device
+    timed, L2 flushed between steps): value, write rate and roofline fraction each."""
+    import torch
+
+    from paper_1707_08213_b200 import _lib
+    from paper_1707_08213_b200.tree2d import _OUT_DTYPES, _precision_code, forward_into
+    from paper_1707_08213_b200.workloads import CONFIGS
+
+    peak, _ = measured_peak()
+    res = {}
+    for name, c in CONFIGS.items():
+        if name == main_cfg.name:
+            continue
+        prec = _precision_code(c.precision, None)
+        x = torch.from_numpy(c.generate()).to(dev)
+        out = torch.empty((c.P0, c.P1, c.n0, c.n1), dtype=_OUT_DTYPES[prec], device=dev)
+        for _ in range(3):
+            forward_into(x, c.m0, c.m1, out, prec=prec, stream=stream)
+        ts = []
+        for _ in range(5):
+            flush_l2(flush)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            forward_into(x, c.m0, c.m1, out, prec=prec, stream=stream)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) / 1e3)
+        t = statistics.median(ts)
+        alg = c.algorithmic_bytes()
+        res[name] = {"desc": c.desc, "dtype": "f32" if prec == _lib.PREC_FP32 else "f64",
+                     "value": c.coefficients / t, "unit": UNIT, "kernel_ms": t * 1e3,
+                     "hbm_write_gbs": c.coefficients * c.out_bytes_per_coef / t / 1e9,
+                     "roofline_frac": alg / t / 1e9 / peak}
+        del x, out
+        torch.cuda.empty_cache()
+    return res
 
 
 def e2e_sharded(args, cfg, x_np, dev, spec, xdt, prec, rank, world):
@@ -442,6 +488,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-others", action="store_true", help="skip the other-configs summary")
     ap.add_argument("--precision", default=None, choices=[None, "fp32", "fp64"],
                     help="override the config's precision (fp64 = DAG-exact complex128)")
     args = ap.parse_args()
