@@ -181,3 +181,58 @@ class SlidingRowStream2D:
 
     def close(self) -> None:
         self.closed = True
+
+
+class SlidingStream1D:
+    """Sample-push 1D stream (tree1d.py:63-119 interface) on the GPU: a device ring of
+    the last n samples (double-stored, so the window is one contiguous view); every push
+    with p >= n - 1 returns the n-point transform of the last n samples (K1 with
+    m0 = 0 over a 1 x n row), bitwise equal to the batch 1D tree in fp64."""
+
+    def __init__(self, spec, counter=None, *, precision="fp64", device=None):
+        if len(spec.exponents) != 1:
+            raise core.ShapeError("SlidingStream1D needs a 1D window spec")
+        (self.m,) = (int(v) for v in spec.exponents)
+        self.n = 1 << self.m
+        self.spec = spec
+        self.counter = counter
+        self.prec = _precision_code(precision, None)
+        self.device = torch.device(device) if device is not None else torch.device(
+            "cuda", torch.cuda.current_device())
+        self._factor = core.normalization_factor(spec)
+        self._ring = torch.zeros(2 * self.n, dtype=_RING_DTYPES[self.prec], device=self.device)
+        self.pushed = 0
+        self.ops_last_push = 0
+        self.closed = False
+
+    def push(self, sample):
+        """Ingest one sample; returns the length-n coefficient vector (device tensor) once
+        the window is full, None while warming up (tree1d.py:92-116)."""
+        if self.closed:
+            raise core.StateError("push after close")
+        p = self.pushed
+        n = self.n
+        slot = p % n
+        v = complex(sample) if not isinstance(sample, torch.Tensor) else sample
+        self._ring[slot] = v
+        self._ring[slot + n] = v
+        ops = 0
+        for l in range(1, self.m + 1):  # tree1d.py:101-108
+            s = 1 << (self.m - l)
+            if p < n - s:
+                break  # higher levels need even more history
+            ops += 1 << l
+            if self.counter is not None:
+                self.counter.add_region((p,), 1 << l, 1)
+        self.ops_last_push = ops
+        self.pushed += 1
+        if p < n - 1:
+            return None
+        first = (p + 1) % n
+        out = torch.empty((1, 1, 1, n), dtype=_OUT_DTYPES[self.prec], device=self.device)
+        forward_into(self._ring[first:first + n].view(1, n), 0, self.m, out, prec=self.prec,
+                     scale=self._factor)
+        return out.view(n)
+
+    def close(self) -> None:
+        self.closed = True

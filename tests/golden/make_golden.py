@@ -211,6 +211,18 @@ def main():
     st = ref_tree2d.SlidingRowStream2D(ref_core.WindowSpec((0, 0)), 6)
     slabs = [st.push_row(r) for r in xs]
     nxt["stream_1x1_sha"] = sha(np.stack(slabs))
+    # the reference's 1D sample-push stream (it works): emitted vectors + per-push ops
+    sig = np.random.default_rng(57).standard_normal(40) + 1j * np.random.default_rng(58).standard_normal(40)
+    c1 = ref_bench.OpCounter((40,))
+    s1 = ref_tree1d.SlidingStream1D(ref_core.WindowSpec((3,), "paper-1d"), counter=c1)
+    outs, ops1 = [], []
+    for v in sig:
+        r = s1.push(v)
+        ops1.append(s1.ops_last_push)
+        if r is not None:
+            outs.append(r)
+    nxt["stream1d"] = {"sha": sha(np.stack(outs)), "ops": ops1, "total": int(c1.total),
+                       "pos_sha": sha(c1.position_ops)}
     nxt["fig4_predict_ops"] = {f"{w}": {a: int(ref_bench.predict_ops(a, (100, 100), (w, w)))
                                         for a in ("tree", "fft", "naive")}
                                for w in (4, 8, 16, 32, 64)}
