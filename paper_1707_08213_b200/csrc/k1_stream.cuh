@@ -79,7 +79,10 @@ template <int M0, int M1, int Q, int TP1, int NBM = 1> struct K1Shape {
     static constexpr int V = n1 / G;                      // values per lane
     static constexpr int GW = 32 / G;                     // transforms per warp task
     static constexpr int TPR = (TP1 + GW - 1) / GW;       // warp tasks per row
-    static constexpr int TASKS = NB * TPR;
+    // n1 > 32: after the in-register level(s) the V slots evolve independently, so a
+    // row transform splits into V warp tasks (one slot each) to spread stage R evenly
+    static constexpr int SPLIT = V > 1 ? V : 1;
+    static constexpr int TASKS = NB * TPR * SPLIT;
     static constexpr int TPW = (TASKS + WARPS - 1) / WARPS;
     static constexpr int NMAX = cmax(n0, n1);
     static constexpr int RING = cmax((M0 - Q) * (n0 / (2 * J)), 1);  // register ring, complex
@@ -175,7 +178,8 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
 #pragma unroll
             for (int tt = 0; tt < S::TPW; ++tt) {
                 const int task = warp + tt * S::WARPS;
-                const int rr = task / TPR, pg = task - rr * TPR;
+                const int t2 = task / S::SPLIT;
+                const int rr = t2 / TPR, pg = t2 - rr * TPR;
                 const int64_t row = brow + rr;
                 const int64_t pcol = pbase + pg * GW + gam;
 #pragma unroll
@@ -208,7 +212,8 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
             for (int tt = 0; tt < S::TPW; ++tt) {
                 const int task = warp + tt * S::WARPS;
                 if ((S::TASKS % S::WARPS) == 0 || task < S::TASKS) {
-                    const int rr = task / TPR, pg = task - rr * TPR;
+                    const int t2 = task / S::SPLIT, bsl = task - t2 * S::SPLIT;  // slot (V > 1)
+                    const int rr = t2 / TPR, pg = t2 - rr * TPR;
                     const int pl = pg * GW + gam;
                     C s[V];
                     if constexpr (TMA) {
@@ -238,32 +243,32 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
 #pragma unroll
                         for (int a = 0; a < V; ++a) s[a] = ns[a];
                     }
+                    // this task's slot (all V slots when the transform is not split)
+                    C sv = s[0];
+#pragma unroll
+                    for (int a = 1; a < V; ++a)
+                        if (bsl == a) sv = s[a];
                     // cross-lane levels: node (c, i) of slot be sits on lane (i/V)*(n1/L) + c
 #pragma unroll
                     for (int L = 2 * V; L <= n1; L *= 2) {
                         const int sL = n1 / L;
                         const int c = lam % sL;
-#pragma unroll
-                        for (int be = 0; be < V; ++be) {
-                            const int i = (lam / sL) * V + be;
-                            const int ip = i % (L / 2);
-                            const int srcE = gam * G + (ip / V) * (2 * sL) + c;
-                            const int srcO = srcE + sL;
-                            C E, O;
-                            E.x = __shfl_sync(0xffffffffu, s[be].x, srcE);
-                            E.y = __shfl_sync(0xffffffffu, s[be].y, srcE);
-                            O.x = __shfl_sync(0xffffffffu, s[be].x, srcO);
-                            O.y = __shfl_sync(0xffffffffu, s[be].y, srcO);
-                            s[be] = bfly<EXACT>(E, tw[i * sL * ST1], O);
-                        }
+                        const int i = (lam / sL) * V + bsl;
+                        const int ip = i % (L / 2);
+                        const int srcE = gam * G + (ip / V) * (2 * sL) + c;
+                        const int srcO = srcE + sL;
+                        C E, O;
+                        E.x = __shfl_sync(0xffffffffu, sv.x, srcE);
+                        E.y = __shfl_sync(0xffffffffu, sv.y, srcE);
+                        O.x = __shfl_sync(0xffffffffu, sv.x, srcO);
+                        O.y = __shfl_sync(0xffffffffu, sv.y, srcO);
+                        sv = bfly<EXACT>(E, tw[i * sL * ST1], O);
                     }
                     if (pl < TP1) {
-                        C *dst = ring + ((b * NB + rr) & (D - 1)) * (TP1 * n1) + pl * n1 + lam * V;
-#pragma unroll
-                        for (int be = 0; be < V; ++be) {
-                            dst[be] = s[be];
-                            dst[be + D * TP1 * n1] = s[be];
-                        }
+                        C *dst = ring + ((b * NB + rr) & (D - 1)) * (TP1 * n1) + pl * n1 +
+                                 lam * V + bsl;
+                        dst[0] = sv;
+                        dst[D * TP1 * n1] = sv;
                     }
                 }
             }
