@@ -120,6 +120,18 @@ def test_config_full_size_fp32(golden, cuda, name):
         assert rel_err(got, ref[None, None]) <= FP32_TOL
         f = np.fft.fft2(x[p0:p0 + cfg.n0, p1:p1 + cfg.n1].astype(np.complex128))
         assert rel_err(got, f[None, None]) <= FP32_TOL
+    # independent check: numpy fft2 of 1024 windows per config —
+    # the four corners, edge midpoints, and seeded random positions
+    rng = np.random.default_rng(int(name[1:]) + 97)
+    pts = [(0, 0), (0, cfg.P1 - 1), (cfg.P0 - 1, 0), (cfg.P0 - 1, cfg.P1 - 1),
+           (cfg.P0 // 2, 0), (0, cfg.P1 // 2), (cfg.P0 - 1, cfg.P1 // 2), (cfg.P0 // 2, cfg.P1 - 1)]
+    pts += list(zip(rng.integers(0, cfg.P0, 1024 - len(pts)), rng.integers(0, cfg.P1, 1024 - len(pts))))
+    p0s = torch.tensor([p[0] for p in pts], device=vals.device)
+    p1s = torch.tensor([p[1] for p in pts], device=vals.device)
+    got = vals[p0s, p1s].cpu().numpy()
+    xw = np.stack([x[a:a + cfg.n0, b:b + cfg.n1] for a, b in pts]).astype(np.complex128)
+    ref_w = np.fft.fft2(xw)
+    assert rel_err(got[None], ref_w[None]) <= FP32_TOL
     # every window: DC coefficient and Parseval, via fp64 summed-area tables on device
     xd = torch.from_numpy(np.ascontiguousarray(x)).to(cuda).to(torch.complex128)
     n0, n1 = cfg.n0, cfg.n1

@@ -129,6 +129,10 @@ def test_wrapper_validation_order(golden):
     # default budget (4 GiB) rejects config 4 exactly as the reference does
     with pytest.raises(BudgetError):
         tree_swdft_2d(np.zeros((4096, 4096), np.float32), WindowSpec((4, 4)))
+    with pytest.raises(WindowTooLargeError):  # empty / ragged extents: check_fits (core.py:116)
+        tree_swdft_2d(np.zeros((0, 5)), WindowSpec((0, 0)))
+    with pytest.raises(ValueError):  # ragged nested lists are not arrays
+        tree_swdft_2d([[1.0, 2.0], [3.0]], WindowSpec((0, 0)))
     with pytest.raises(ValueError):  # np.asarray(x, complex128) fails first (tree2d.py:189)
         tree_swdft_2d(np.array([["a", "b"], ["c", "d"]]), WindowSpec((1, 1)))
 
