@@ -366,20 +366,33 @@ const K1Info *k1_info() {
 }
 
 // Shape per (m0, m1): J = 2^Q residue groups so that each thread emits n0/J = 4
-// coefficients per row (Q = m0 - 2), capped at 512 threads per window column;
-// TP1 window columns per CTA so that a CTA is ~128 threads.  Measured on B200
-// with scripts/tune (profiles/TUNING_r01.md): e.g. c4 (16x16) Q=2/TP1=2 831
-// Gcoef/s vs 760 for Q=1/TP1=8; c3 (32x8) Q=3/TP1=2 783; c5 (64x64) Q=3/TP1=1 797.
-// fp64-exact (DBL) butterflies cost ~2x and run without FMA, so the chain that
-// rebuilds the level-Q node (2^Q - 1 butterflies per row) is capped at Q = 2 for
-// m0 = 5 (c3 in fp64: 369 Gcoef/s at Q=2 vs 243 at Q=3, profiles/TUNING_r01.md).
+// coefficients per row (Q = m0 - 2, at most 3: the level-Q chain costs 2^Q - 1
+// butterflies per row), capped at 512 threads per window column; TP1 window columns
+// per CTA so that a CTA is ~128 threads.  Shapes where the sweep over all windows
+// 4..64 x 4..64 (profiles/SWEEP_r01.md) found a >3 % faster (Q, TP1) use that instead
+// (fp32).  fp64-exact (DBL) butterflies cost ~2x and run without FMA, so m0 = 5 uses
+// Q = 2 there (c3 in fp64: 369 Gcoef/s at Q=2 vs 243 at Q=3).
+struct K1Choice {
+    int m0, m1, q, tp1;
+};
+constexpr K1Choice K1_TUNED_FP32[] = {
+    {2, 3, 0, 32}, {3, 2, 0, 64}, {3, 4, 1, 2}, {4, 3, 2, 8}, {4, 6, 1, 1}, {5, 2, 3, 8},
+    {5, 4, 3, 2},  {5, 6, 2, 1},  {6, 2, 3, 2}, {6, 3, 3, 2}, {6, 4, 3, 1}, {6, 5, 3, 1},
+};
 constexpr int k1_choose_q(int M0, int M1, bool DBL = false) {
+    if (!DBL)
+        for (const K1Choice &c : K1_TUNED_FP32)
+            if (c.m0 == M0 && c.m1 == M1) return c.q;
     int q = M0 > 2 ? M0 - 2 : 0;
+    if (q > 3) q = 3;
     if (DBL && M0 == 5) q = 2;
     while (q > 0 && (1 << M1) * (1 << q) > 512) --q;
     return q;
 }
-constexpr int k1_choose_tp1(int M1, int Q) {
+constexpr int k1_choose_tp1(int M0, int M1, int Q, bool DBL = false) {
+    if (!DBL)
+        for (const K1Choice &c : K1_TUNED_FP32)
+            if (c.m0 == M0 && c.m1 == M1) return c.tp1;
     const int per = (1 << M1) * (1 << Q);
     return per >= 128 ? 1 : 128 / per;
 }
@@ -387,7 +400,7 @@ constexpr int k1_choose_tp1(int M1, int Q) {
 template <int M0, int M1, bool DBL> struct K1Inst {
     using T = typename std::conditional<DBL, double, float>::type;
     static constexpr int Q = k1_choose_q(M0, M1, DBL);
-    static constexpr int TP1 = k1_choose_tp1(M1, Q);
+    static constexpr int TP1 = k1_choose_tp1(M0, M1, Q, DBL);
     using S = K1Shape<M0, M1, Q, TP1>;
     static void reg() {
         register_k1(k1_info<T, M0, M1, Q, TP1, DBL>());
