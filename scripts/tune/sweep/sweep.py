@@ -28,6 +28,7 @@ def rule_q(M0, M1):
 
 
 def main():
+    prec = int(sys.argv[1]) if len(sys.argv) > 1 else 0  # 0: fp32 variants, 1: fp64-exact
     lib = ctypes.CDLL(os.path.join(HERE, "_build", "libsweep.so"))
     lib.tune_name.restype = ctypes.c_char_p
     for name, (res, args) in _lib.SIGNATURES.items():
@@ -38,19 +39,22 @@ def main():
     s = torch.cuda.current_stream(dev)
     by_shape = {}
     for v in range(lib.tune_count()):
-        by_shape.setdefault((lib.tune_m(v, 0), lib.tune_m(v, 1)), []).append(v)
+        if lib.tune_m(v, 4) == prec:
+            by_shape.setdefault((lib.tune_m(v, 0), lib.tune_m(v, 1)), []).append(v)
     for (m0, m1), vs in sorted(by_shape.items()):
         n0, n1 = 1 << m0, 1 << m1
-        N = int(min(8192, max(4 * max(n0, n1), math.sqrt(8e9 / (8 * n0 * n1)))))
+        ob = 16 if prec else 8
+        N = int(min(8192, max(4 * max(n0, n1), math.sqrt(8e9 / (ob * n0 * n1)))))
         x = torch.randn((N, N), device=dev, dtype=torch.float32)
         P0, P1 = N - n0 + 1, N - n1 + 1
-        out = torch.empty((P0, P1, n0, n1), dtype=torch.complex64, device=dev)
+        out = torch.empty((P0, P1, n0, n1), dtype=torch.complex128 if prec else torch.complex64,
+                          device=dev)
         coefs = P0 * P1 * n0 * n1
         for v in vs:
             lib.tune_select(v)
 
             def launch():
-                rc = lib.swdft2d_forward(x.data_ptr(), 0, N, N, N, m0, m1, 0, 1.0, 0, P0,
+                rc = lib.swdft2d_forward(x.data_ptr(), 0, N, N, N, m0, m1, prec, 1.0, 0, P0,
                                          out.data_ptr(), 1, s.cuda_stream)
                 assert rc == 0, lib.swdft2d_last_error()
 
@@ -72,7 +76,7 @@ def main():
             rule_tp1 = max(1, 128 // (n1 << rule_q(m0, m1)))
             print(json.dumps({"m0": m0, "m1": m1, "N": N, "Q": q, "TP1": tp1,
                               "threads": lib.tune_m(v, 2), "gcoef_s": coefs / t / 1e9,
-                              "write_tbs": coefs * 8 / t / 1e12,
+                              "write_tbs": coefs * ob / t / 1e12, "prec": prec,
                               "is_rule": q == rule_q(m0, m1) and tp1 == rule_tp1}), flush=True)
         del x, out
         torch.cuda.empty_cache()

@@ -12,8 +12,8 @@ void k1_register_m0_3() {}
 void k1_register_m0_4() {}
 void k1_register_m0_5() {}
 void k1_register_m0_6() {}
-extern const Variant SWEEP_2[], SWEEP_3[], SWEEP_4[], SWEEP_5[], SWEEP_6[];
-static const Variant *ALL[] = {SWEEP_2, SWEEP_3, SWEEP_4, SWEEP_5, SWEEP_6};
+extern const Variant SWEEP_2[], SWEEP_3[], SWEEP_4[], SWEEP_5[], SWEEP_6[], SWEEP64[];
+static const Variant *ALL[] = {SWEEP_2, SWEEP_3, SWEEP_4, SWEEP_5, SWEEP_6, SWEEP64};
 static const Variant *nth(int v) {
     for (const Variant *a : ALL)
         for (; a->name; ++a)
@@ -30,7 +30,8 @@ extern "C" int tune_count(void) {
 extern "C" const char *tune_name(int v) { return swdft2d::nth(v)->name; }
 extern "C" int tune_m(int v, int which) {
     const swdft2d::K1Info *i = swdft2d::nth(v)->info();
-    return which == 0 ? i->m0 : which == 1 ? i->m1 : which == 2 ? i->threads : (int)i->smem_bytes;
+    return which == 0 ? i->m0 : which == 1 ? i->m1 : which == 2 ? i->threads :
+           which == 4 ? i->prec : (int)i->smem_bytes;
 }
 extern "C" int tune_select(int v) {
     swdft2d::find_k1(0, 0, 0);
