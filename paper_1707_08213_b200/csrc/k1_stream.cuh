@@ -370,8 +370,9 @@ const K1Info *k1_info() {
 // butterflies per row), capped at 512 threads per window column; TP1 window columns
 // per CTA so that a CTA is ~128 threads.  Shapes where the sweep over all windows
 // 4..64 x 4..64 (profiles/SWEEP_r01.md) found a >3 % faster (Q, TP1) use that instead
-// (fp32).  fp64-exact (DBL) butterflies cost ~2x and run without FMA, so m0 = 5 uses
-// Q = 2 there (c3 in fp64: 369 Gcoef/s at Q=2 vs 243 at Q=3).
+// (fp32).  fp64-exact (DBL) butterflies cost ~2x and run without FMA: the fp64 sweep
+// picked Q = 2 for m0 = 3..5 (c3 in fp64: 369 Gcoef/s at Q=2 vs 243 at Q=3; 8x8: 317
+// vs 292 at Q=1).
 struct K1Choice {
     int m0, m1, q, tp1;
 };
@@ -379,20 +380,23 @@ constexpr K1Choice K1_TUNED_FP32[] = {
     {2, 3, 0, 32}, {3, 2, 0, 64}, {3, 4, 1, 2}, {4, 3, 2, 8}, {4, 6, 1, 1}, {5, 2, 3, 8},
     {5, 4, 3, 2},  {5, 6, 2, 1},  {6, 2, 3, 2}, {6, 3, 3, 2}, {6, 4, 3, 1}, {6, 5, 3, 1},
 };
+constexpr K1Choice K1_TUNED_FP64[] = {{3, 4, 1, 2}};
 constexpr int k1_choose_q(int M0, int M1, bool DBL = false) {
-    if (!DBL)
-        for (const K1Choice &c : K1_TUNED_FP32)
-            if (c.m0 == M0 && c.m1 == M1) return c.q;
+    for (const K1Choice &c : K1_TUNED_FP32)
+        if (!DBL && c.m0 == M0 && c.m1 == M1) return c.q;
+    for (const K1Choice &c : K1_TUNED_FP64)
+        if (DBL && c.m0 == M0 && c.m1 == M1) return c.q;
     int q = M0 > 2 ? M0 - 2 : 0;
     if (q > 3) q = 3;
-    if (DBL && M0 == 5) q = 2;
+    if (DBL && M0 >= 3 && M0 <= 5) q = 2;  // fp64 sweep: Q = 2 best for m0 = 3, 4, 5
     while (q > 0 && (1 << M1) * (1 << q) > 512) --q;
     return q;
 }
 constexpr int k1_choose_tp1(int M0, int M1, int Q, bool DBL = false) {
-    if (!DBL)
-        for (const K1Choice &c : K1_TUNED_FP32)
-            if (c.m0 == M0 && c.m1 == M1) return c.tp1;
+    for (const K1Choice &c : K1_TUNED_FP32)
+        if (!DBL && c.m0 == M0 && c.m1 == M1) return c.tp1;
+    for (const K1Choice &c : K1_TUNED_FP64)
+        if (DBL && c.m0 == M0 && c.m1 == M1) return c.tp1;
     const int per = (1 << M1) * (1 << Q);
     return per >= 128 ? 1 : 128 / per;
 }
