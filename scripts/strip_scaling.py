@@ -11,7 +11,6 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
-from paper_1707_08213_b200 import _lib  # noqa: E402
 from paper_1707_08213_b200.partition import strip_plan  # noqa: E402
 from paper_1707_08213_b200.tree2d import _OUT_DTYPES, _precision_code, forward_into  # noqa: E402
 from paper_1707_08213_b200.workloads import CONFIGS  # noqa: E402

@@ -2,7 +2,6 @@
 shapes / windows / dtypes against the pinned oracle (fp64 bitwise)."""
 import numpy as np
 import pytest
-import torch
 from hypothesis import HealthCheck, given, settings
 from hypothesis import strategies as st
 

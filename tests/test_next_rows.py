@@ -2,7 +2,6 @@
 verify + bench CSV, 1D tree.  CPU tests cover the host-only parts; GPU tests go
 through libswdft2d.so."""
 import hashlib
-import os
 
 import numpy as np
 import pytest
