@@ -79,3 +79,24 @@ def test_fp32_accuracy_bound_large_values(cuda, oracle_lib):
         ref = oracle_lib.tree2d(x.astype(np.float64), *m)
         got = run(x, m, precision="fp32")
         assert oracle.window_rel_err(got, ref) <= 1e-4
+
+
+def test_special_values_fp64(cuda, oracle_lib):
+    """Infinities, NaNs, signed zeros and subnormals flow through the device tree exactly
+    as through the reference's arithmetic: identical bits wherever the result is not
+    NaN, and NaN in exactly the same places."""
+    rng = np.random.default_rng(9)
+    x = rng.standard_normal((24, 20))
+    x[3, 4] = np.inf
+    x[10, 11] = -np.inf
+    x[15, 2] = np.nan
+    x[5, 15] = -0.0
+    x[20, 7] = 5e-324
+    x[0, 0] = 2.2250738585072014e-308 / 3
+    for m in [(2, 2), (3, 1), (1, 3)]:
+        ref = oracle_lib.tree2d(x, *m)
+        for kernel in ("auto", "window"):
+            got = run(x, m, kernel=kernel)
+            rn, gn = np.isnan(ref.view(np.float64)), np.isnan(got.view(np.float64))
+            assert np.array_equal(rn, gn)
+            assert np.array_equal(ref.view(np.uint64)[~rn], got.view(np.uint64)[~gn])
