@@ -122,15 +122,57 @@ def forward_into(xt: torch.Tensor, m0: int, m1: int, out: torch.Tensor, *, prec:
     return out
 
 
+def _forward_to_host(xt, m0, m1, host, prec, scale, kernel, strip_bytes, slots=4, copiers=2):
+    """Out-of-core variant: window rows in strips of ~strip_bytes, computed into a ring of
+    `slots` device buffers and copied to the pinned host array `host` on `copiers` copy
+    streams while the next strips compute.  Device memory: slots * strip_bytes."""
+    dev = xt.device
+    P0, P1, n0, n1 = host.shape
+    row_bytes = P1 * n0 * n1 * host.element_size()
+    rows = max(1, min(P0, strip_bytes // max(1, row_bytes)))
+    ring = [torch.empty((rows, P1, n0, n1), dtype=host.dtype, device=dev)
+            for _ in range(min(slots, -(-P0 // rows)))]
+    comp = torch.cuda.current_stream(dev)
+    copy = [torch.cuda.Stream(dev) for _ in range(copiers)]
+    freed = [None] * len(ring)  # event: the slot's previous strip has left the device
+    for k, a in enumerate(range(0, P0, rows)):
+        b = min(P0, a + rows)
+        slot = k % len(ring)
+        if freed[slot] is not None:
+            comp.wait_event(freed[slot])
+        buf = ring[slot][:b - a]
+        forward_into(xt, m0, m1, buf, prec=prec, scale=scale, p0_begin=a, p0_end=b,
+                     kernel=kernel, stream=comp)
+        done = torch.cuda.Event()
+        done.record(comp)
+        cs = copy[k % copiers]
+        cs.wait_event(done)
+        with torch.cuda.stream(cs):
+            host[a:b].copy_(buf, non_blocking=True)
+        freed[slot] = torch.cuda.Event()
+        freed[slot].record(cs)
+        buf.record_stream(cs)
+    for cs in copy:
+        comp.wait_stream(cs)
+    comp.synchronize()
+    return host
+
+
 def tree_swdft_2d(x, spec, loop_order: str = "levels-outer", counter=None, budget=None,
                   threads: int = 1, *, precision=None, device=None, out=None,
-                  kernel: str = "auto") -> CoefficientArray:
+                  kernel: str = "auto", to_host: bool = False, host_out=None,
+                  strip_bytes: int = 1 << 29) -> CoefficientArray:
     """Sliding-window 2D DFT via the shared-tree algorithm, on a B200.
 
     Equals the reference's tree_swdft_2d bit for bit with precision="fp64" and
     to <= 1e-4 of each window's L2 norm with precision="fp32".  The budget check
     uses the reference's own accounting (lattice + output at 16 B/complex,
     tree2d.py:195-196) and runs before anything is allocated.
+
+    ``values`` is a device tensor by default; ``to_host=True`` (or a pinned
+    ``host_out`` tensor) returns a numpy array as the reference does, streaming
+    strips of ~``strip_bytes`` device->host while later strips compute, so the
+    device holds only a few strips of output.
     """
     xt = _to_tensor(x)
     if xt.dim() != 2 or len(spec.exponents) != 2:
@@ -152,9 +194,22 @@ def tree_swdft_2d(x, spec, loop_order: str = "levels-outer", counter=None, budge
         xt = xt.to(device, non_blocking=xt.is_pinned() if not xt.is_cuda else False)
     n0, n1 = 1 << m0, 1 << m1
     P0, P1 = shape[0] - n0 + 1, shape[1] - n1 + 1
+    scale = core.normalization_factor(spec)
+    if to_host or host_out is not None:
+        # host (numpy) output, as the reference returns: strips computed in a small
+        # device ring and streamed to pinned host memory while the next strips compute
+        want = (P0, P1, n0, n1)
+        if host_out is None:
+            host_out = torch.empty(want, dtype=_OUT_DTYPES[prec], pin_memory=True)
+        if tuple(host_out.shape) != want or host_out.dtype != _OUT_DTYPES[prec] or \
+                host_out.is_cuda:
+            raise ValueError(f"host_out must be a host {_OUT_DTYPES[prec]} tensor of shape {want}")
+        _forward_to_host(xt, m0, m1, host_out, prec, scale, kernel, strip_bytes)
+        if counter is not None:
+            replay_counter(counter, shape, spec)
+        return CoefficientArray(host_out.numpy(), shape, spec, spec.normalization)
     if out is None:
         out = torch.empty((P0, P1, n0, n1), dtype=_OUT_DTYPES[prec], device=device)
-    scale = core.normalization_factor(spec)
     forward_into(xt, m0, m1, out, prec=prec, scale=scale, kernel=kernel)
     if counter is not None:
         replay_counter(counter, shape, spec)

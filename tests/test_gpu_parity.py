@@ -311,3 +311,20 @@ def test_large_windows_k0_and_unsupported(cuda, oracle_lib):
     y = np.zeros((2048, 2))
     with pytest.raises(UnsupportedError):
         run(y, 11, 0, "fp64")                                     # beyond K0's 2^10
+
+
+def test_host_output_pipeline(cuda, oracle_lib):
+    """to_host / host_out: strips computed in a device ring and streamed to pinned host
+    memory equal the device-resident result bit for bit (fp64), with many strips."""
+    rng = np.random.default_rng(13)
+    x = rng.standard_normal((70, 50)) + 1j * rng.standard_normal((70, 50))
+    ref = oracle_lib.tree2d(x, 3, 2)
+    res = tree_swdft_2d(x, WindowSpec((3, 2)), precision="fp64", to_host=True,
+                        strip_bytes=3 * 47 * 32 * 16)  # 3 window rows per strip -> 21 strips
+    assert isinstance(res.values, np.ndarray)
+    assert bits_equal(res.values, ref)
+    host = torch.empty((63, 47, 8, 4), dtype=torch.complex64, pin_memory=True)
+    res32 = tree_swdft_2d(x.astype(np.complex64), WindowSpec((3, 2)), host_out=host,
+                          strip_bytes=1 << 12)
+    assert res32.values.base is not None or res32.values.ctypes.data == host.data_ptr()
+    assert rel_err(res32.values, ref) <= FP32_TOL
