@@ -19,9 +19,12 @@ Default workload: config 4 (4096x4096 f32 image-like array, 16x16 windows,
   cpu_baseline  the C restatement of the reference (oracle/, all host threads)
              on the first window rows of the same config (rank 0, N=1 only)
 
-N > 1 (torchrun, one process per GPU, NCCL): rank 0 holds the input in HBM;
-each step = scatter of input row strips with halos (NCCL send/recv from rank 0)
-+ every rank's strip of the transform; time = max over ranks; strong scaling.
+N > 1 (torchrun, one process per GPU, NCCL), --scaling weak (default): every rank
+transforms its own config-sized workload (generated locally) with no data-path
+collective; value = N x coefficients / (max over ranks of the step time).
+--scaling strong: ONE workload partitioned into window-row strips; rank 0 holds
+the input in HBM and each step = pipelined scatter of input row strips with
+halos (NCCL send/recv from rank 0) + every rank's strip of the transform.
 
 --impl reference: times the CPU reference path (the oracle's C restatement of
 the reference's levels-outer tree, all host threads) on a bounded sample of the
@@ -180,7 +183,8 @@ def run_reference(args, cfg, rank):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": 1e3 * tot / len(times), "higher_is_better": True,
+        "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json recipe)",
         "config": {"workload": cfg.name, "desc": cfg.desc, "sample_window_rows": rows},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
@@ -211,28 +215,32 @@ def run_ours(args, cfg, rank, world, local_rank):
     stream = torch.cuda.current_stream(dev)
     flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
 
-    x_np = cfg.generate() if rank == 0 else None
+    # N > 1 modes: "weak" (default) — every rank transforms its own full workload (its
+    # own share of window rows of an N-times taller array, generated locally): no
+    # data-path collective, per-GPU work fixed.  "strong" — the north-star partition of
+    # ONE workload: window-row strips scattered from rank 0 over NCCL (pipelined).
+    strips = world > 1 and args.scaling == "strong"
+    x_np = cfg.generate() if (rank == 0 or not strips) else None
     xdt = {"float32": torch.float32, "float64": torch.float64, "complex64": torch.complex64,
            "complex128": torch.complex128}[cfg.dtype]
     P0, P1, n0, n1 = cfg.P0, cfg.P1, cfg.n0, cfg.n1
-    plan = strip_plan(P0, cfg.m0, world)
-    a, b, rb, re = plan[rank]
+    plan = strip_plan(P0, cfg.m0, world if strips else 1)
+    a, b, rb, re = plan[rank if strips else 0]
     out = torch.empty((b - a, P1, n0, n1), dtype=odt, device=dev)
-    if rank == 0:
-        x_full = torch.from_numpy(x_np).to(dev)
-    recv = None if rank == 0 else torch.empty((re - rb, cfg.N1), dtype=xdt, device=dev)
+    x_full = torch.from_numpy(x_np).to(dev) if x_np is not None else None
+    recv = torch.empty((re - rb, cfg.N1), dtype=xdt, device=dev) if x_full is None else None
 
     pieces = choose_pieces((cfg.N0, cfg.N1), cfg.m0, cfg.m1, np.dtype(cfg.dtype).itemsize,
-                           out.element_size(), world)
+                           out.element_size(), world) if strips else 1
 
     def compute(local, w0, w1):
         forward_into(local, cfg.m0, cfg.m1, out[w0:w1], prec=prec, p0_begin=w0, p0_end=w1,
                      stream=stream)
 
     def step():
-        # N > 1: the partitioner's pipelined scatter — every strip travels from rank 0 in
-        # two in-order chunks and each rank starts on its first (1/8) chunk on arrival
-        if world > 1:
+        # strong: the partitioner's pipelined scatter — every strip travels from rank 0 in
+        # in-order chunks and each rank starts on its first chunk on arrival
+        if strips:
             pipelined_strip_forward(x_full if rank == 0 else None, (cfg.N0, cfg.N1), cfg.m0, xdt,
                                     dev, compute, recv=recv, pieces=pieces)
         elif b > a:
@@ -244,7 +252,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         step()
     torch.cuda.synchronize()
     graph = None
-    if world == 1 and not args.no_graph:
+    if not strips and not args.no_graph:
         # one step = one K1 launch; replaying it from a CUDA graph keeps host-side
         # launch overhead out of the device-timed region
         graph = torch.cuda.CUDAGraph()
@@ -280,7 +288,8 @@ def run_ours(args, cfg, rank, world, local_rank):
     else:
         t_job = t_local
     step_s = t_job / args.steps
-    value = cfg.coefficients / step_s
+    units = cfg.coefficients * (world if (world > 1 and not strips) else 1)
+    value = units / step_s
     out_bpc = 8 if prec == _lib.PREC_FP32 else 16
     bytes_alg = cfg.coefficients * out_bpc + cfg.in_bytes
 
@@ -289,14 +298,14 @@ def run_ours(args, cfg, rank, world, local_rank):
     kern_s = step_s
 
     peak, peak_src = measured_peak()
-    achieved = bytes_alg / kern_s / 1e9 if world == 1 else (
+    achieved = bytes_alg / kern_s / 1e9 if not strips else (
         ((b - a) * P1 * n0 * n1 * out_bpc + (re - rb) * cfg.N1 * np.dtype(cfg.dtype).itemsize)
         / (t_local / args.steps) / 1e9)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None,
+        "scaling": args.scaling, "vs_baseline": None,
         "dtype": "f32" if prec == _lib.PREC_FP32 else "f64",
         "data": "synthetic (seeded, BASELINE.json recipe; see paper_1707_08213_b200/workloads.py)",
         "config": {"workload": cfg.name, "desc": cfg.desc, "N0": cfg.N0, "N1": cfg.N1,
@@ -304,9 +313,11 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "output_bytes": cfg.coefficients * out_bpc,
                    "l2": "256 MiB flush write between timed steps (outside the events); "
                          "output >> L2 as well",
-                   "parallelism": f"strips{world}" if world > 1 else "single",
+                   "parallelism": (f"strips{world} (NCCL scatter from rank 0)" if strips else
+                                   f"replicas{world} (each rank its own full workload, no "
+                                   "data-path collective)" if world > 1 else "single"),
                    "scatter_pieces": pieces},
-        "hbm_write_gbs": cfg.coefficients * out_bpc / step_s / 1e9,
+        "hbm_write_gbs": units * out_bpc / step_s / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": ncu_traffic(cfg.name),
                      "peak_source": peak_src,
@@ -314,13 +325,13 @@ def run_ours(args, cfg, rank, world, local_rank):
         "kernel": dict(_lib.stream_kernel_info(cfg.m0, cfg.m1, prec), name="K1 k1_stream_kernel"),
         "clocks": clk.summary(),
         # K1 launches per step: one at N=1; up to `pieces` per rank under the pipelined scatter
-        "gpu_launches": args.steps * (1 if world == 1 else pieces),
+        "gpu_launches": args.steps * pieces,
     }
 
     # e2e through the public API from pinned host memory
     if not args.no_e2e:
-        if world == 1:
-            line["e2e"] = e2e_host(args, cfg, x_np, dev, spec, odt, out)
+        if not strips:
+            line["e2e"] = e2e_host(args, cfg, x_np, dev, spec, odt, out, world)
         else:
             del out
             torch.cuda.empty_cache()
@@ -434,17 +445,30 @@ def e2e_sharded(args, cfg, x_np, dev, spec, xdt, prec, rank, world):
                     "to its own pinned host buffer; max over ranks"}
 
 
-def e2e_host(args, cfg, x_np, dev, spec, odt, out_dev):
-    """tree_swdft_2d(host x) -> device -> full coefficient array back in pinned host memory."""
+def e2e_host(args, cfg, x_np, dev, spec, odt, out_dev, world=1):
+    """tree_swdft_2d(host x) -> device -> full coefficient array back in pinned host memory
+    (every rank its own workload when world > 1; time = max over ranks)."""
     import torch
 
     from paper_1707_08213_b200 import tree_swdft_2d
 
+    need = out_dev.numel() * out_dev.element_size() + x_np.nbytes
+    if world > 1:
+        # every rank pins its own full output: make sure the host can hold N of them
+        import psutil
+
+        ok = torch.tensor([float(psutil.virtual_memory().available > 1.25 * world * need)],
+                          dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(ok, op=torch.distributed.ReduceOp.MIN)
+        if not ok.item():
+            return {"skipped": f"host RAM < {world} x {need / 1e9:.0f} GB pinned outputs"}
     x_pin = torch.from_numpy(x_np).pin_memory()
     host_out = torch.empty(out_dev.shape, dtype=odt, pin_memory=True)
     stream = torch.cuda.current_stream(dev)
     times = []
     for i in range(args.warmup + args.e2e_steps):
+        if world > 1:
+            torch.distributed.barrier()
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -455,11 +479,17 @@ def e2e_host(args, cfg, x_np, dev, spec, odt, out_dev):
         if i >= args.warmup:
             times.append(e0.elapsed_time(e1) / 1e3)
     s = statistics.mean(times)
+    if world > 1:
+        tt = torch.tensor([s], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        s = float(tt.item())
     # the same call with the coefficients left resident in HBM (a GPU consumer's view):
     # H2D of the input, the transform, and a D2H read of one window's coefficients
     win = torch.empty(out_dev.shape[2:], dtype=odt, pin_memory=True)
     rtimes = []
     for i in range(args.warmup + args.e2e_steps):
+        if world > 1:
+            torch.distributed.barrier()
         torch.cuda.synchronize()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
@@ -471,13 +501,17 @@ def e2e_host(args, cfg, x_np, dev, spec, odt, out_dev):
         if i >= args.warmup:
             rtimes.append(e0.elapsed_time(e1) / 1e3)
     r = statistics.mean(rtimes)
-    return {"value": cfg.coefficients / s, "unit": UNIT,
+    if world > 1:
+        tt = torch.tensor([r], dtype=torch.float64, device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        r = float(tt.item())
+    return {"value": world * cfg.coefficients / s, "unit": UNIT,
             "h2d_bytes_per_step": int(x_pin.numel() * x_pin.element_size()),
             "d2h_bytes_per_step": int(host_out.numel() * host_out.element_size()),
             "ms_per_step": s * 1e3, "steps": len(times),
             "path": "tree_swdft_2d(pinned host input, host_out=pinned): strips computed in a "
                     "device ring and copied D2H on 2 copy streams while later strips compute",
-            "resident": {"value": cfg.coefficients / r, "unit": UNIT, "ms_per_step": r * 1e3,
+            "resident": {"value": world * cfg.coefficients / r, "unit": UNIT, "ms_per_step": r * 1e3,
                          "h2d_bytes_per_step": int(x_pin.numel() * x_pin.element_size()),
                          "d2h_bytes_per_step": int(win.numel() * win.element_size()),
                          "path": "same call, coefficients left in HBM, one window read back"}}
@@ -496,6 +530,9 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-others", action="store_true", help="skip the other-configs summary")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N>1: weak = every rank its own workload, no collective (default); "
+                         "strong = one workload in strips scattered from rank 0 over NCCL")
     ap.add_argument("--precision", default=None, choices=[None, "fp32", "fp64"],
                     help="override the config's precision (fp64 = DAG-exact complex128)")
     args = ap.parse_args()
