@@ -124,6 +124,39 @@ int swdft2d_stream_kernel_info(int m0, int m1, int prec, int64_t info[6]);
  */
 int swdft2d_strip_range(int64_t P0, int m0, int rank, int world, int64_t range[4]);
 
+/*
+ * Single-process multi-GPU forward (SURVEY.md 8b "swdft2d_forward_multi", 8e): the
+ * strip partition above over ndev devices driven from one host thread.  The reference
+ * has no multi-device path; its axis-0 chunking is tree2d.py:22-27,58-64.
+ *   x         device pointer on devs[0] (N0 x N1, row stride ld_x), ready on streams[0]
+ *   devs      CUDA device ordinals; slot g owns strip g of ndev (duplicates allowed)
+ *   stage[g]  g >= 1: buffer on devs[g] of (row_end - row_begin) x N1 elements of
+ *             in_dtype (rows contiguous, ld = N1) that receives strip g with its
+ *             n0-1 halo rows; stage[0] (and stage itself when ndev == 1) is unused
+ *   outs[g]   buffer on devs[g] of (p0_end - p0_begin) x P1 x n0 x n1 complex of prec
+ *   streams[g] cudaStream_t on devs[g]
+ * Per slot g >= 1: streams[g] waits for x, copies the strip over NVLink (peer access is
+ * enabled on first use; cudaMemcpyDefault), then runs swdft2d_forward on the stage.
+ * Slot 0 computes straight from x.  Work later enqueued on streams[0] is ordered after
+ * every strip copy, so x may be reused from there.  Nothing is allocated on the device;
+ * outputs stay on their devices (no gather, no reduction).
+ */
+int swdft2d_forward_multi(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t ld_x,
+                          int m0, int m1, int prec, double scale, int ndev, const int *devs,
+                          void *const *stage, void *const *outs, void *const *streams);
+
+/*
+ * One push of the row-push stream (SlidingRowStream2D.push_row, tree2d.py:205-303,
+ * SPEC.md:335-343): store row p0 (device pointer, N1 elements of in_dtype) into the
+ * device ring ([2 n0, N1] complex of prec; row p lives at slots p mod n0 and
+ * p mod n0 + n0), then, once p0 >= n0 - 1, write window row p0 - n0 + 1's
+ * (P1, n0, n1) slab to out — equal (bitwise in fp64) to that row of the batch
+ * transform.  Rows must be pushed in order 0, 1, 2, ...; out may be NULL while
+ * p0 < n0 - 1.  Two stream-ordered launches (ring store, K1 over the ring view).
+ */
+int swdft2d_stream_push(const void *row, int in_dtype, int64_t N1, void *ring, int m0, int m1,
+                        int prec, double scale, int64_t p0, void *out, int kernel, void *stream);
+
 /* Frees cached per-device state (twiddle tables).  Safe to call twice. */
 int swdft2d_shutdown(void);
 

@@ -45,6 +45,11 @@ SIGNATURES = {
     "swdft2d_has_stream_kernel": (_int, [_int, _int, _int]),
     "swdft2d_stream_kernel_info": (_int, [_int, _int, _int, _pi64]),
     "swdft2d_strip_range": (_int, [_i64, _int, _int, _int, _pi64]),
+    "swdft2d_forward_multi": (_int, [_vp, _int, _i64, _i64, _i64, _int, _int, _int, _dbl, _int,
+                                     ctypes.POINTER(ctypes.c_int), ctypes.POINTER(_vp),
+                                     ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
+    "swdft2d_stream_push": (_int, [_vp, _int, _i64, _vp, _int, _int, _int, _dbl, _i64, _vp, _int,
+                                   _vp]),
     "swdft2d_shutdown": (_int, []),
 }
 

@@ -14,6 +14,7 @@
 #include <mutex>
 #include <string>
 #include <utility>
+#include <vector>
 
 #include <cudaTypedefs.h>
 
@@ -289,7 +290,7 @@ int swdft2d_twiddles(int n, double *out) {
 
 int swdft2d_has_stream_kernel(int m0, int m1, int prec) { return find_k1(m0, m1, prec) ? 1 : 0; }
 
-int swdft2d_stream_kernel_info(int m0, int m1, int prec, int64_t info[4]) {
+int swdft2d_stream_kernel_info(int m0, int m1, int prec, int64_t info[6]) {
     const K1Info *k = find_k1(m0, m1, prec);
     if (!k) return fail(SWDFT2D_E_UNSUPPORTED, "no K1 instantiation for m0=%d m1=%d prec=%d", m0, m1, prec);
     if (!info) return fail(SWDFT2D_E_INVALID_ARG, "null info");
@@ -411,6 +412,127 @@ int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(SWDFT2D_E_CUDA, "kernel launch: %s", cudaGetErrorString(e));
     return SWDFT2D_OK;
+}
+
+static const int64_t k_in_bytes[4] = {4, 8, 8, 16};  // SWDFT2D_IN_* element sizes
+
+// Peer access from `dev` to `src` (once per pair; a no-op where the pair has no P2P —
+// cudaMemcpyDefault then stages through the host).
+static void enable_peer(int dev, int src) {
+    static std::mutex mu;
+    static std::map<std::pair<int, int>, bool> done;
+    std::lock_guard<std::mutex> lk(mu);
+    auto key = std::make_pair(dev, src);
+    if (dev == src || done.count(key)) return;
+    int can = 0;
+    cudaDeviceCanAccessPeer(&can, dev, src);
+    if (can) {
+        cudaSetDevice(dev);
+        if (cudaDeviceEnablePeerAccess(src, 0) == cudaErrorPeerAccessAlreadyEnabled)
+            cudaGetLastError();
+    }
+    done[key] = true;
+}
+
+int swdft2d_forward_multi(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t ld_x,
+                          int m0, int m1, int prec, double scale, int ndev, const int *devs,
+                          void *const *stage, void *const *outs, void *const *streams) {
+    if (ndev < 1 || !devs || !outs || !streams)
+        return fail(SWDFT2D_E_INVALID_ARG, "forward_multi: need ndev >= 1 devices, outs and streams");
+    if (in_dtype < SWDFT2D_IN_F32 || in_dtype > SWDFT2D_IN_C128)
+        return fail(SWDFT2D_E_INVALID_ARG, "unknown input dtype code %d", in_dtype);
+    if (N0 < 1 || N1 < 1) return fail(SWDFT2D_E_SHAPE, "empty input (%lld x %lld)", (long long)N0, (long long)N1);
+    if (ld_x < N1) return fail(SWDFT2D_E_INVALID_ARG, "ld_x %lld < N1 %lld", (long long)ld_x, (long long)N1);
+    int64_t P0 = 0, P1 = 0;
+    int rc = swdft2d_output_shape(N0, N1, m0, m1, &P0, &P1);
+    if (rc) return rc;
+    if (!x) return fail(SWDFT2D_E_INVALID_ARG, "null device pointer");
+    int cur = 0;
+    cudaGetDevice(&cur);
+    const int64_t es = k_in_bytes[in_dtype];
+    // x is ready on devs[0]'s stream: every other device's stream waits for it, copies its
+    // strip (with halo) into its own stage buffer, and computes there
+    cudaEvent_t ready = nullptr;
+    cudaSetDevice(devs[0]);
+    cudaError_t e = cudaEventCreateWithFlags(&ready, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventRecord(ready, reinterpret_cast<cudaStream_t>(streams[0]));
+    if (e != cudaSuccess) {
+        if (ready) cudaEventDestroy(ready);
+        cudaSetDevice(cur);
+        return fail(SWDFT2D_E_CUDA, "forward_multi: event on device %d: %s", devs[0], cudaGetErrorString(e));
+    }
+    std::vector<cudaEvent_t> copied;
+    for (int g = 0; g < ndev && rc == SWDFT2D_OK; ++g) {
+        int64_t r[4];
+        if ((rc = swdft2d_strip_range(P0, m0, g, ndev, r))) break;
+        if (r[1] == r[0]) continue;
+        cudaStream_t st = reinterpret_cast<cudaStream_t>(streams[g]);
+        if (g == 0) {
+            cudaSetDevice(devs[0]);
+            rc = swdft2d_forward(x, in_dtype, N0, N1, ld_x, m0, m1, prec, scale, r[0], r[1],
+                                 outs[0], SWDFT2D_KERNEL_AUTO, streams[0]);
+            continue;
+        }
+        if (!stage || !stage[g] || !outs[g]) {
+            rc = fail(SWDFT2D_E_INVALID_ARG, "forward_multi: device slot %d needs a stage and an out buffer", g);
+            break;
+        }
+        enable_peer(devs[g], devs[0]);
+        cudaSetDevice(devs[g]);
+        const int64_t rows = r[3] - r[2];
+        e = cudaStreamWaitEvent(st, ready, 0);
+        if (e == cudaSuccess)
+            e = cudaMemcpy2DAsync(stage[g], (size_t)(N1 * es),
+                                  static_cast<const char *>(x) + r[2] * ld_x * es, (size_t)(ld_x * es),
+                                  (size_t)(N1 * es), (size_t)rows, cudaMemcpyDefault, st);
+        cudaEvent_t ev = nullptr;
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventRecord(ev, st);
+        if (ev) copied.push_back(ev);
+        if (e != cudaSuccess) {
+            rc = fail(SWDFT2D_E_CUDA, "forward_multi: strip copy to device %d: %s", devs[g],
+                      cudaGetErrorString(e));
+            break;
+        }
+        rc = swdft2d_forward(stage[g], in_dtype, rows, N1, N1, m0, m1, prec, scale, 0, r[1] - r[0],
+                             outs[g], SWDFT2D_KERNEL_AUTO, streams[g]);
+    }
+    // later work on devs[0]'s stream (e.g. overwriting x) is ordered after every strip copy
+    cudaSetDevice(devs[0]);
+    for (cudaEvent_t ev : copied) {
+        cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(streams[0]), ev, 0);
+        cudaEventDestroy(ev);
+    }
+    cudaEventDestroy(ready);
+    cudaSetDevice(cur);
+    return rc;
+}
+
+int swdft2d_stream_push(const void *row, int in_dtype, int64_t N1, void *ring, int m0, int m1,
+                        int prec, double scale, int64_t p0, void *out, int kernel, void *stream) {
+    if (in_dtype < SWDFT2D_IN_F32 || in_dtype > SWDFT2D_IN_C128)
+        return fail(SWDFT2D_E_INVALID_ARG, "unknown input dtype code %d", in_dtype);
+    if (prec != SWDFT2D_PREC_FP32 && prec != SWDFT2D_PREC_FP64)
+        return fail(SWDFT2D_E_INVALID_ARG, "unknown precision code %d", prec);
+    if (p0 < 0) return fail(SWDFT2D_E_INVALID_ARG, "negative row index %lld", (long long)p0);
+    if (m0 < 0 || m1 < 0 || m0 > 30) return fail(SWDFT2D_E_INVALID_WINDOW, "bad window exponents");
+    const int64_t n0 = (int64_t)1 << m0;
+    int rc = swdft2d_output_shape(n0, N1, m0, m1, nullptr, nullptr);
+    if (rc) return rc;
+    if (!row || !ring) return fail(SWDFT2D_E_INVALID_ARG, "null device pointer");
+    DeviceState *ds = nullptr;
+    if ((rc = device_state(&ds))) return rc;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    launch_ring_store(row, in_dtype, N1, ring, prec, (int)n0, p0, ds->sms, st);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(SWDFT2D_E_CUDA, "ring store: %s", cudaGetErrorString(e));
+    if (p0 < n0 - 1) return SWDFT2D_OK;  // warming up: no window row complete yet
+    if (!out) return fail(SWDFT2D_E_INVALID_ARG, "null output slab");
+    const int64_t first = (p0 + 1) % n0;
+    const int64_t eb = prec == SWDFT2D_PREC_FP64 ? 16 : 8;
+    const void *win = static_cast<const char *>(ring) + first * N1 * eb;
+    return swdft2d_forward(win, prec == SWDFT2D_PREC_FP64 ? SWDFT2D_IN_C128 : SWDFT2D_IN_C64, n0,
+                           N1, N1, m0, m1, prec, scale, 0, 1, out, kernel, stream);
 }
 
 int swdft2d_shutdown(void) {

@@ -51,4 +51,9 @@ void register_k1(const K1Info *info);
 
 int launch_k0(const K0Params &P, int prec, cudaStream_t stream);
 
+// Stream ring: store row p0 (N1 elements of in_dtype) at slots p0 mod n0 and
+// p0 mod n0 + n0 of ring ([2 n0, N1] complex of prec).
+int launch_ring_store(const void *row, int in_dtype, int64_t N1, void *ring, int prec, int n0,
+                      int64_t p0, int sms, cudaStream_t stream);
+
 }  // namespace swdft2d

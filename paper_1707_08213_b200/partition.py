@@ -214,3 +214,61 @@ def tree_swdft_2d_sharded(x, spec, *, shape=None, dtype=None, group=None, src: i
 
     pipelined_strip_forward(x, shape, m0, dtype, device, compute, group, src, pieces=pieces)
     return ShardedCoefficients(out, a, b, tuple(shape), spec, spec.normalization)
+
+
+def tree_swdft_2d_multi(x, spec, devices, *, precision=None, budget=None):
+    """Single-process multi-GPU tree_swdft_2d over ``devices`` (swdft2d_forward_multi).
+
+    ``x`` is a CUDA tensor on devices[0] (or host data, copied there).  Device slot g
+    gets strip g of len(devices) (swdft2d_strip_range): its input rows are copied over
+    NVLink into a stage buffer on that device and transformed there; slot 0 computes
+    straight from x.  Returns one ShardedCoefficients per slot, each resident on its
+    device, in strip order — the same shards the torchrun path returns per rank.
+    Stream-ordered on every device's current torch stream.  Budget accounting is the
+    reference's, for the whole problem (tree2d.py:195-196).
+    """
+    import ctypes
+
+    from .tree2d import _IN_CODES, _OUT_DTYPES, _precision_code, _to_tensor
+
+    devs = [torch.device(d) if not isinstance(d, int) else torch.device("cuda", d)
+            for d in devices]
+    if not devs or any(d.type != "cuda" for d in devs):
+        raise ValueError("devices must be a non-empty list of CUDA devices")
+    devs = [torch.device("cuda", d.index if d.index is not None else torch.cuda.current_device())
+            for d in devs]
+    xt = _to_tensor(x)
+    if xt.dim() != 2 or len(spec.exponents) != 2:
+        raise core.ShapeError("tree_swdft_2d expects a 2D array and 2D window")
+    shape = (int(xt.shape[0]), int(xt.shape[1]))
+    spec.check_fits(shape)
+    core.check_budget(core.lattice_bytes(shape, spec) + core.output_bytes(shape, spec), budget,
+                      what="level buffers + coefficient output")
+    if xt.device != devs[0]:
+        xt = xt.to(devs[0])
+    if xt.stride(1) != 1:
+        xt = xt.contiguous()
+    m0, m1 = (int(m) for m in spec.exponents)
+    prec = _precision_code(precision, xt.dtype)
+    n0, n1 = 1 << m0, 1 << m1
+    P0, P1 = shape[0] - n0 + 1, shape[1] - n1 + 1
+    G = len(devs)
+    plan = strip_plan(P0, m0, G)
+    outs, stages = [], []
+    for g, (a, b, rb, re) in enumerate(plan):
+        outs.append(torch.empty((b - a, P1, n0, n1), dtype=_OUT_DTYPES[prec], device=devs[g]))
+        stages.append(torch.empty((re - rb, shape[1]), dtype=xt.dtype, device=devs[g])
+                      if g > 0 else None)
+    streams = [torch.cuda.current_stream(d) for d in devs]
+    vp = ctypes.c_void_p
+    c_devs = (ctypes.c_int * G)(*[d.index for d in devs])
+    c_stage = (vp * G)(*[None if t is None or t.numel() == 0 else t.data_ptr() for t in stages])
+    c_outs = (vp * G)(*[t.data_ptr() if t.numel() else None for t in outs])
+    c_streams = (vp * G)(*[s.cuda_stream for s in streams])
+    rc = _lib.load().swdft2d_forward_multi(xt.data_ptr(), _IN_CODES[xt.dtype], shape[0], shape[1],
+                                           xt.stride(0), m0, m1, prec,
+                                           float(core.normalization_factor(spec)), G, c_devs,
+                                           c_stage, c_outs, c_streams)
+    _lib.check(rc)
+    return [ShardedCoefficients(outs[g], a, b, shape, spec, spec.normalization)
+            for g, (a, b, _, _) in enumerate(plan)]

@@ -21,7 +21,7 @@ import numpy as np
 import torch
 
 from . import _lib, core
-from .tree2d import _OUT_DTYPES, _precision_code, forward_into
+from .tree2d import _IN_CODES, _OUT_DTYPES, _precision_code, _to_tensor, forward_into
 
 _RING_DTYPES = {_lib.PREC_FP32: torch.complex64, _lib.PREC_FP64: torch.complex128}
 
@@ -45,7 +45,11 @@ class SlidingRowStream2D:
         self.device = torch.device(device) if device is not None else torch.device(
             "cuda", torch.cuda.current_device())
         self.kernel = kernel
-        self._factor = core.normalization_factor(spec)
+        if kernel not in _lib.KERNELS:
+            raise ValueError(f"kernel must be one of {tuple(_lib.KERNELS)}")
+        self._kernel_code = _lib.KERNELS[kernel]
+        self._lib = _lib.load()
+        self._factor = float(core.normalization_factor(spec))
         self._ring = torch.zeros((2 * self.n0, self.N1), dtype=_RING_DTYPES[self.prec],
                                  device=self.device)
         self.P1 = self.N1 - self.n1 + 1
@@ -111,35 +115,34 @@ class SlidingRowStream2D:
             self.ops_last_push = ops
             np.copyto(self.last_push_position_ops, vec)
 
-    def _store(self, p0: int, r: torch.Tensor) -> None:
-        slot = p0 % self.n0
-        self._ring[slot].copy_(r)
-        self._ring[slot + self.n0].copy_(r)
-
     def push_row(self, row):
         """Ingest one length-N1 row; returns the (P1, n0, n1) slab (device tensor)
-        once n0 rows have arrived, None while warming up."""
+        once n0 rows have arrived, None while warming up.  One C-ABI call
+        (swdft2d_stream_push: ring store + K1 over the ring view)."""
         if self.closed:
             raise core.StateError("push after close")
-        if isinstance(row, torch.Tensor):
-            r = row
-        else:
-            r = torch.from_numpy(np.asarray(row, dtype=np.complex128))
+        r = _to_tensor(row)
         if tuple(r.shape) != (self.N1,):
             raise core.ShapeError(f"row shape {tuple(r.shape)} != ({self.N1},)")
+        if r.device != self.device:
+            r = r.to(self.device, non_blocking=(not r.is_cuda) and r.is_pinned())
+        if r.stride(0) != 1:
+            r = r.contiguous()
         p0 = self.rows_pushed
-        n0, n1 = self.n0, self.n1
-        self._store(p0, r.to(device=self.device, dtype=self._ring.dtype))
+        n0 = self.n0
+        slab = None
+        if p0 >= n0 - 1:
+            slab = torch.empty((self.P1, n0, self.n1), dtype=_OUT_DTYPES[self.prec],
+                               device=self.device)
+        with torch.cuda.device(self.device):
+            rc = self._lib.swdft2d_stream_push(
+                r.data_ptr(), _IN_CODES[r.dtype], self.N1, self._ring.data_ptr(), self.m0, self.m1,
+                self.prec, self._factor, p0, slab.data_ptr() if slab is not None else None,
+                self._kernel_code, torch.cuda.current_stream(self.device).cuda_stream)
+        _lib.check(rc)
         self._account(p0)
         self.rows_pushed += 1
-        if p0 < n0 - 1:
-            return None
-        first = (p0 + 1) % n0
-        window_rows = self._ring[first:first + n0]
-        slab = torch.empty((1, self.P1, n0, n1), dtype=_OUT_DTYPES[self.prec], device=self.device)
-        forward_into(window_rows, self.m0, self.m1, slab, prec=self.prec, scale=self._factor,
-                     kernel=self.kernel)
-        return slab[0]
+        return slab
 
     def push_rows(self, rows):
         """Ingest k rows at once (a [k, N1] block); returns the [k', P1, n0, n1] slabs
@@ -165,8 +168,9 @@ class SlidingRowStream2D:
             for i in range(k - 1):
                 self._account(first + i, last=False)
         self._account(first + k - 1)
-        for i in range(max(0, k - n0), k):  # keep the last n0 rows for later pushes
-            self._store(first + i, blk[i])
+        keep = min(k, n0)  # keep the last n0 rows for later pushes (both ring copies)
+        slots = torch.arange(first + k - keep, first + k, device=self.device) % n0
+        self._ring.index_copy_(0, torch.cat([slots, slots + n0]), blk[k - keep:].repeat(2, 1))
         self.rows_pushed += k
         w_begin = max(0, first - n0 + 1)  # global window rows completed by this block
         w_end = first + k - n0 + 1

@@ -1,7 +1,8 @@
 """Drop-in B200 replacement for the reference's batch 2D tree SWDFT.
 
     tree_swdft_2d(x, spec, loop_order="levels-outer", counter=None, budget=None,
-                  threads=1, *, precision=None, device=None, out=None, kernel="auto")
+                  threads=1, *, precision=None, device=None, out=None, kernel="auto",
+                  devices=None)
 
 mirrors /root/reference/pkg/src/swdft/tree2d.py:175-202: same arguments, the
 same validation order and exceptions, the same [P0, P1, n0, n1] layout, twiddle
@@ -161,7 +162,7 @@ def _forward_to_host(xt, m0, m1, host, prec, scale, kernel, strip_bytes, slots=4
 def tree_swdft_2d(x, spec, loop_order: str = "levels-outer", counter=None, budget=None,
                   threads: int = 1, *, precision=None, device=None, out=None,
                   kernel: str = "auto", to_host: bool = False, host_out=None,
-                  strip_bytes: int = 1 << 29) -> CoefficientArray:
+                  strip_bytes: int = 1 << 29, devices=None):
     """Sliding-window 2D DFT via the shared-tree algorithm, on a B200.
 
     Equals the reference's tree_swdft_2d bit for bit with precision="fp64" and
@@ -173,6 +174,10 @@ def tree_swdft_2d(x, spec, loop_order: str = "levels-outer", counter=None, budge
     ``host_out`` tensor) returns a numpy array as the reference does, streaming
     strips of ~``strip_bytes`` device->host while later strips compute, so the
     device holds only a few strips of output.
+
+    ``devices=[d0, d1, ...]`` splits the window rows into one strip per device from
+    this one process (partition.tree_swdft_2d_multi) and returns the
+    list of per-device ShardedCoefficients with their [p0_begin, p0_end) ranges.
     """
     xt = _to_tensor(x)
     if xt.dim() != 2 or len(spec.exponents) != 2:
@@ -183,6 +188,13 @@ def tree_swdft_2d(x, spec, loop_order: str = "levels-outer", counter=None, budge
         raise ValueError(f"loop_order must be one of {LOOP_ORDERS}")
     required = core.lattice_bytes(shape, spec) + core.output_bytes(shape, spec)
     core.check_budget(required, budget, what="level buffers + coefficient output")
+    if devices is not None:
+        from .partition import tree_swdft_2d_multi
+
+        shards = tree_swdft_2d_multi(xt, spec, devices, precision=precision, budget=budget)
+        if counter is not None:
+            replay_counter(counter, shape, spec)
+        return shards
     if kernel not in _lib.KERNELS:
         raise ValueError(f"kernel must be one of {tuple(_lib.KERNELS)}")
     m0, m1 = _spec_exponents(spec)

@@ -272,6 +272,71 @@ def test_strip_partition_on_device(cuda, world):
         assert torch.equal(part.view(torch.float64), full[a:b].view(torch.float64))
 
 
+@pytest.mark.gpu
+@pytest.mark.parametrize("slots,dtype", [(1, np.float64), (3, np.float64), (8, np.float32),
+                                         (4, np.complex128)])
+def test_forward_multi_slots(cuda, oracle_lib, slots, dtype):
+    """swdft2d_forward_multi / tree_swdft_2d(devices=[...]): every device slot's shard
+    equals its rows of the single-device output bitwise (fp64) and, for fp32, of the
+    same K1 run; the union covers [0, P0) in order.  One GPU box: all slots on cuda:0
+    (the strip copy is then a device-local cudaMemcpy2DAsync, the same call)."""
+    from paper_1707_08213_b200 import OpCounter
+
+    rng = np.random.default_rng(slots)
+    x = rng.standard_normal((67, 45))
+    if dtype is np.complex128:
+        x = x + 1j * rng.standard_normal((67, 45))
+    x = x.astype(dtype)
+    spec = WindowSpec((3, 2), "unitary")
+    xt = torch.from_numpy(x).to(cuda)
+    # a strided row view exercises ld_x > N1 in the strip copies
+    wide = torch.zeros((67, 53), dtype=xt.dtype, device=cuda)
+    wide[:, :45] = xt
+    full = tree_swdft_2d(xt, spec, budget=1 << 40).values
+    c1, c2 = OpCounter((67, 45)), OpCounter((67, 45))
+    shards = tree_swdft_2d(wide[:, :45], spec, budget=1 << 40, devices=[0] * slots, counter=c1)
+    tree_swdft_2d(x, spec, budget=1 << 40, counter=c2)
+    assert c1.total == c2.total
+    torch.cuda.synchronize()
+    assert len(shards) == slots
+    assert shards[0].p0_begin == 0 and shards[-1].p0_end == full.shape[0]
+    for g, sh in enumerate(shards):
+        if g:
+            assert sh.p0_begin == shards[g - 1].p0_end
+        fl = torch.float64 if full.dtype == torch.complex128 else torch.float32
+        assert torch.equal(sh.values.view(fl), full[sh.p0_begin:sh.p0_end].view(fl))
+    if dtype is not np.float32:
+        from paper_1707_08213_b200.core import normalization_factor
+
+        ref = oracle_lib.tree2d(x, 3, 2, scale=normalization_factor(spec))
+        got = torch.cat([sh.values for sh in shards]).cpu().numpy()
+        assert np.array_equal(got.view(np.float64), ref.view(np.float64))
+
+
+@pytest.mark.gpu
+def test_forward_multi_errors(cuda):
+    """Missing stage/out buffers and bad arguments fail loudly with the ABI's codes."""
+    import ctypes
+
+    lib = _lib.load()
+    xt = torch.zeros((16, 16), dtype=torch.float32, device=cuda)
+    out = torch.empty((5, 5, 4, 4), dtype=torch.complex64, device=cuda)
+    s = torch.cuda.current_stream(cuda).cuda_stream
+    vp = ctypes.c_void_p
+    devs = (ctypes.c_int * 2)(0, 0)
+    rc = lib.swdft2d_forward_multi(xt.data_ptr(), 0, 16, 16, 16, 2, 2, 0, 1.0, 2, devs,
+                                   (vp * 2)(None, None), (vp * 2)(out.data_ptr(), None),
+                                   (vp * 2)(s, s))
+    assert rc == _lib.E_INVALID_ARG and b"stage" in lib.swdft2d_last_error()
+    rc = lib.swdft2d_forward_multi(xt.data_ptr(), 0, 16, 16, 16, 2, 2, 0, 1.0, 0, devs,
+                                   None, None, None)
+    assert rc == _lib.E_INVALID_ARG
+    rc = lib.swdft2d_forward_multi(xt.data_ptr(), 0, 16, 16, 16, 5, 2, 0, 1.0, 1, devs,
+                                   None, (vp * 1)(out.data_ptr()), (vp * 1)(s))
+    assert rc == _lib.E_WINDOW_TOO_LARGE
+    torch.cuda.synchronize()
+
+
 def test_sharded_api_world1(cuda):
     """tree_swdft_2d_sharded through a real NCCL process group of size 1 equals tree_swdft_2d."""
     import os
