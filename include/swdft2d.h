@@ -147,15 +147,25 @@ int swdft2d_forward_multi(const void *x, int in_dtype, int64_t N0, int64_t N1, i
 
 /*
  * One push of the row-push stream (SlidingRowStream2D.push_row, tree2d.py:205-303,
- * SPEC.md:335-343): store row p0 (device pointer, N1 elements of in_dtype) into the
- * device ring ([2 n0, N1] complex of prec; row p lives at slots p mod n0 and
- * p mod n0 + n0), then, once p0 >= n0 - 1, write window row p0 - n0 + 1's
- * (P1, n0, n1) slab to out — equal (bitwise in fp64) to that row of the batch
- * transform.  Rows must be pushed in order 0, 1, 2, ...; out may be NULL while
- * p0 < n0 - 1.  Two stream-ordered launches (ring store, K1 over the ring view).
+ * SPEC.md:335-343).  Rows must be pushed in order p0 = 0, 1, 2, ...; once
+ * p0 >= n0 - 1 the (P1, n0, n1) slab of window row p0 - n0 + 1 is written to out
+ * (equal, bitwise in fp64, to that row of the batch transform).
+ *   row    device pointer, N1 elements of in_dtype
+ *   state  incremental mode (m0, m1 <= SWDFT2D_K1_MAX_M): the tree's level state,
+ *          swdft2d_stream_state_bytes bytes, zero-filled before the first push.  One
+ *          K2 launch computes the pushed row's dim-1 tree nodes and the dim-0 levels
+ *          from the state — the reference stream's O(n0 n1) work per position.
+ *          NULL: recompute mode, K1 (or `kernel`) over the raw ring.
+ *   ring   raw row ring, [2 n0, N1] complex of prec (row p at slots p mod n0 and
+ *          p mod n0 + n0); required in recompute mode, optional (may be NULL) with state
+ *   out    may be NULL while p0 < n0 - 1 (or to only advance the state)
  */
-int swdft2d_stream_push(const void *row, int in_dtype, int64_t N1, void *ring, int m0, int m1,
-                        int prec, double scale, int64_t p0, void *out, int kernel, void *stream);
+int swdft2d_stream_push(const void *row, int in_dtype, int64_t N1, void *ring, void *state, int m0,
+                        int m1, int prec, double scale, int64_t p0, void *out, int kernel,
+                        void *stream);
+
+/* Bytes of the incremental stream state: (m0 * n0/2 + n0 - 1) * P1 * n1 complex of prec. */
+int swdft2d_stream_state_bytes(int64_t N1, int m0, int m1, int prec, int64_t *bytes);
 
 /* Frees cached per-device state (twiddle tables).  Safe to call twice. */
 int swdft2d_shutdown(void);

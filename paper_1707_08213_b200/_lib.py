@@ -26,6 +26,7 @@ E_CUDA = -7
 E_NOMEM = -8
 
 IN_F32, IN_F64, IN_C64, IN_C128 = 0, 1, 2, 3
+K1_MAX_M, K0_MAX_M = 6, 10  # SWDFT2D_K1_MAX_M / SWDFT2D_K0_MAX_M
 PREC_FP32, PREC_FP64 = 0, 1
 KERNEL_AUTO, KERNEL_STREAM, KERNEL_WINDOW, KERNEL_STREAM_TMA = 0, 1, 2, 3
 KERNELS = {"auto": KERNEL_AUTO, "stream": KERNEL_STREAM, "window": KERNEL_WINDOW,
@@ -48,8 +49,9 @@ SIGNATURES = {
     "swdft2d_forward_multi": (_int, [_vp, _int, _i64, _i64, _i64, _int, _int, _int, _dbl, _int,
                                      ctypes.POINTER(ctypes.c_int), ctypes.POINTER(_vp),
                                      ctypes.POINTER(_vp), ctypes.POINTER(_vp)]),
-    "swdft2d_stream_push": (_int, [_vp, _int, _i64, _vp, _int, _int, _int, _dbl, _i64, _vp, _int,
-                                   _vp]),
+    "swdft2d_stream_push": (_int, [_vp, _int, _i64, _vp, _vp, _int, _int, _int, _dbl, _i64, _vp,
+                                   _int, _vp]),
+    "swdft2d_stream_state_bytes": (_int, [_i64, _int, _int, _int, _pi64]),
     "swdft2d_shutdown": (_int, []),
 }
 

@@ -144,6 +144,19 @@ static void host_twiddles(int n, double *re, double *im) {
     }
 }
 
+// make_twiddles(64) as double2, computed once (every K1/K2 launch passes it by value)
+static const double2 *k1_twiddles() {
+    static const struct Table {
+        double2 t[K1_TW_N];
+        Table() {
+            double re[K1_TW_N], im[K1_TW_N];
+            host_twiddles(K1_TW_N, re, im);
+            for (int i = 0; i < K1_TW_N; ++i) t[i] = make_double2(re[i], im[i]);
+        }
+    } table;
+    return table.t;
+}
+
 static int device_state(DeviceState **out) {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
@@ -379,9 +392,7 @@ int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t
             if (v > 0) P.RCH = v < rows ? v : rows;
         }
         P.ntiles = P.CB * ((rows + P.RCH - 1) / P.RCH);
-        double re[K1_TW_N], im[K1_TW_N];
-        host_twiddles(K1_TW_N, re, im);
-        for (int i = 0; i < K1_TW_N; ++i) P.tw[i] = make_double2(re[i], im[i]);
+        std::memcpy(P.tw, k1_twiddles(), sizeof P.tw);
         const int64_t grid = P.ntiles < slots ? P.ntiles : slots;
         k1->launch(P, tmap, (int)grid, st);
     } else {
@@ -508,21 +519,62 @@ int swdft2d_forward_multi(const void *x, int in_dtype, int64_t N0, int64_t N1, i
     return rc;
 }
 
-int swdft2d_stream_push(const void *row, int in_dtype, int64_t N1, void *ring, int m0, int m1,
-                        int prec, double scale, int64_t p0, void *out, int kernel, void *stream) {
+int swdft2d_stream_state_bytes(int64_t N1, int m0, int m1, int prec, int64_t *bytes) {
+    if (prec != SWDFT2D_PREC_FP32 && prec != SWDFT2D_PREC_FP64)
+        return fail(SWDFT2D_E_INVALID_ARG, "unknown precision code %d", prec);
+    if (!bytes) return fail(SWDFT2D_E_INVALID_ARG, "null output");
+    if (m0 < 0 || m1 < 0 || m0 > SWDFT2D_K1_MAX_M || m1 > SWDFT2D_K1_MAX_M)
+        return fail(SWDFT2D_E_UNSUPPORTED, "no incremental stream kernel for m0=%d m1=%d", m0, m1);
+    int64_t P1 = 0;
+    int rc = swdft2d_output_shape((int64_t)1 << m0, N1, m0, m1, nullptr, &P1);
+    if (rc) return rc;
+    const int64_t eb = prec == SWDFT2D_PREC_FP64 ? 16 : 8;
+    const int64_t n0 = (int64_t)1 << m0;
+    const int64_t nodes = m0 ? (int64_t)m0 * (n0 / 2) + n0 - 1 : 0;  // per column, k2_push.cu
+    *bytes = nodes * P1 * ((int64_t)1 << m1) * eb;
+    return SWDFT2D_OK;
+}
+
+int swdft2d_stream_push(const void *row, int in_dtype, int64_t N1, void *ring, void *state, int m0,
+                        int m1, int prec, double scale, int64_t p0, void *out, int kernel,
+                        void *stream) {
     if (in_dtype < SWDFT2D_IN_F32 || in_dtype > SWDFT2D_IN_C128)
         return fail(SWDFT2D_E_INVALID_ARG, "unknown input dtype code %d", in_dtype);
     if (prec != SWDFT2D_PREC_FP32 && prec != SWDFT2D_PREC_FP64)
         return fail(SWDFT2D_E_INVALID_ARG, "unknown precision code %d", prec);
+    if (kernel < SWDFT2D_KERNEL_AUTO || kernel > SWDFT2D_KERNEL_STREAM_TMA)
+        return fail(SWDFT2D_E_INVALID_ARG, "unknown kernel code %d", kernel);
     if (p0 < 0) return fail(SWDFT2D_E_INVALID_ARG, "negative row index %lld", (long long)p0);
     if (m0 < 0 || m1 < 0 || m0 > 30) return fail(SWDFT2D_E_INVALID_WINDOW, "bad window exponents");
     const int64_t n0 = (int64_t)1 << m0;
-    int rc = swdft2d_output_shape(n0, N1, m0, m1, nullptr, nullptr);
+    int64_t P1 = 0;
+    int rc = swdft2d_output_shape(n0, N1, m0, m1, nullptr, &P1);
     if (rc) return rc;
-    if (!row || !ring) return fail(SWDFT2D_E_INVALID_ARG, "null device pointer");
+    if (!row || (!ring && !state)) return fail(SWDFT2D_E_INVALID_ARG, "null device pointer");
     DeviceState *ds = nullptr;
     if ((rc = device_state(&ds))) return rc;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (state) {  // K2: incremental push over the level state (and the raw ring, if given)
+        if (m0 > SWDFT2D_K1_MAX_M || m1 > SWDFT2D_K1_MAX_M)
+            return fail(SWDFT2D_E_UNSUPPORTED, "no incremental stream kernel for m0=%d m1=%d", m0, m1);
+        K2Params P;
+        std::memset(&P, 0, sizeof P);
+        P.row = row;
+        P.in_dtype = in_dtype;
+        P.apply_scale = scale == 1.0 ? 0 : 1;
+        P.N1 = N1;
+        P.P1 = P1;
+        P.r = p0;
+        P.state = state;
+        P.ring = ring;
+        P.out = p0 >= n0 - 1 ? out : nullptr;
+        P.scale = scale;
+        std::memcpy(P.tw, k1_twiddles(), sizeof P.tw);
+        launch_k2(P, m0, m1, prec, st);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return fail(SWDFT2D_E_CUDA, "K2 push: %s", cudaGetErrorString(e));
+        return SWDFT2D_OK;
+    }
     launch_ring_store(row, in_dtype, N1, ring, prec, (int)n0, p0, ds->sms, st);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(SWDFT2D_E_CUDA, "ring store: %s", cudaGetErrorString(e));

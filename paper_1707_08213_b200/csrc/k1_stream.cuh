@@ -51,16 +51,6 @@
 
 namespace swdft2d {
 
-// Compile-time loop: f(std::integral_constant<int, I>) for I = 0..N-1, so every
-// register-array index inside f is a constant (keeps rings/accumulators in registers).
-template <typename F, int... Is>
-__device__ __forceinline__ void static_for_impl(F &&f, std::integer_sequence<int, Is...>) {
-    (f(std::integral_constant<int, Is>{}), ...);
-}
-template <int N, typename F> __device__ __forceinline__ void static_for(F &&f) {
-    static_for_impl(f, std::make_integer_sequence<int, N>{});
-}
-
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 __host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
 constexpr int pow2ceil(int v) {

@@ -51,6 +51,20 @@ void register_k1(const K1Info *info);
 
 int launch_k0(const K0Params &P, int prec, cudaStream_t stream);
 
+// K2: one incremental stream push (k2_push.cu).
+struct K2Params {
+    const void *row;  // the pushed row, N1 elements of in_dtype
+    int in_dtype, apply_scale;
+    int64_t N1, P1;
+    int64_t r;    // index of the pushed row
+    void *state;  // (m0 * n0/2 + n0 - 1) * P1 * n1 complex (level rings), zero-initialised
+    void *ring;   // optional raw ring [2 n0, N1] (nullptr: not stored)
+    void *out;    // optional (P1, n0, n1) slab of window row r - n0 + 1
+    double scale;
+    double2 tw[K1_TW_N];
+};
+int launch_k2(const K2Params &P, int m0, int m1, int prec, cudaStream_t stream);
+
 // Stream ring: store row p0 (N1 elements of in_dtype) at slots p0 mod n0 and
 // p0 mod n0 + n0 of ring ([2 n0, N1] complex of prec).
 int launch_ring_store(const void *row, int in_dtype, int64_t N1, void *ring, int prec, int n0,

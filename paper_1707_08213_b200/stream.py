@@ -8,14 +8,21 @@ equals the batch transform's rows exactly.  The reference's
 implementation raises for every window larger than 1x1;
 this one implements the specified behaviour.
 
-Device state: the last n0 input rows in a double-stored ring (row p lives at
-slots p mod n0 and p mod n0 + n0), so the n0 rows a window row needs are always
-one contiguous [n0, N1] view; each push with p0 >= n0 - 1 runs the K1 kernel
-over that view for exactly one window row (bitwise equal to the batch output
-in fp64).  Operation accounting (``ops_last_push``, ``last_push_position_ops``,
+Device state, as the reference's stream keeps its tree levels between pushes:
+the column levels of the dim-0 tree (m0 * n0/2 complex per output column, one
+ring per level) advanced by one K2 launch per push (``swdft2d_stream_push``
+with a state buffer: the pushed row's dim-1 nodes plus the dim-0 levels, O(n0 n1)
+per window position, bitwise equal to the batch output in fp64).  Also the last
+n0 input rows in a double-stored ring (row p at slots p mod n0 and p mod n0 + n0,
+one contiguous [n0, N1] view): ``push_rows`` runs K1 over a block plus the n0 - 1
+rows before it, and the next single push re-derives the level state from the
+ring.  With an explicit ``kernel`` (or windows beyond 64) a push instead re-runs
+that kernel over the ring view for the one window row.  Operation accounting (``ops_last_push``, ``last_push_position_ops``,
 ``counter.add_region``) follows tree2d.py:251-293 call for call.
 """
 from __future__ import annotations
+
+import ctypes
 
 import numpy as np
 import torch
@@ -52,12 +59,24 @@ class SlidingRowStream2D:
         self._factor = float(core.normalization_factor(spec))
         self._ring = torch.zeros((2 * self.n0, self.N1), dtype=_RING_DTYPES[self.prec],
                                  device=self.device)
+        # incremental mode (K2): the tree's column-level state, advanced by every push
+        self._state = None
+        if kernel == "auto" and max(self.m0, self.m1) <= _lib.K1_MAX_M:
+            nbytes = ctypes.c_int64()
+            _lib.check(self._lib.swdft2d_stream_state_bytes(self.N1, self.m0, self.m1, self.prec,
+                                                            ctypes.byref(nbytes)))
+            self._state = torch.zeros(max(1, nbytes.value), dtype=torch.uint8, device=self.device)
+        self._state_rows = 0  # rows the state has absorbed (== rows_pushed unless push_rows ran)
+        self._ring_ptr = self._ring.data_ptr()
+        self._dev_index = self.device.index if self.device.index is not None else \
+            torch.cuda.current_device()
         self.P1 = self.N1 - self.n1 + 1
         self._levels = self._level_plan()
         self._profiles = self._push_profiles()
         self.rows_pushed = 0
         self.ops_last_push = 0
         self.last_push_position_ops = np.zeros(self.N1, dtype=np.int64)
+        self._last_profile = -1
         self.closed = False
 
     def _level_plan(self):
@@ -111,14 +130,18 @@ class SlidingRowStream2D:
                         break  # deeper column levels need even more rows
                     self.counter.add_region((p0, slice(n1 - 1, N1)), nodes, N1 - n1 + 1)
         if last:
-            ops, vec = self._profiles[self._col_levels_run(p0)]
+            k = self._col_levels_run(p0) if p0 < n0 - 1 else self.m0
+            ops, vec = self._profiles[k]
             self.ops_last_push = ops
-            np.copyto(self.last_push_position_ops, vec)
+            if k != self._last_profile:  # the array only changes while warming up
+                np.copyto(self.last_push_position_ops, vec)
+                self._last_profile = k
 
     def push_row(self, row):
         """Ingest one length-N1 row; returns the (P1, n0, n1) slab (device tensor)
         once n0 rows have arrived, None while warming up.  One C-ABI call
-        (swdft2d_stream_push: ring store + K1 over the ring view)."""
+        (swdft2d_stream_push: one K2 launch over the level state, or, with an explicit
+        kernel, the ring store + that kernel over the ring view)."""
         if self.closed:
             raise core.StateError("push after close")
         r = _to_tensor(row)
@@ -134,15 +157,40 @@ class SlidingRowStream2D:
         if p0 >= n0 - 1:
             slab = torch.empty((self.P1, n0, self.n1), dtype=_OUT_DTYPES[self.prec],
                                device=self.device)
-        with torch.cuda.device(self.device):
-            rc = self._lib.swdft2d_stream_push(
-                r.data_ptr(), _IN_CODES[r.dtype], self.N1, self._ring.data_ptr(), self.m0, self.m1,
-                self.prec, self._factor, p0, slab.data_ptr() if slab is not None else None,
-                self._kernel_code, torch.cuda.current_stream(self.device).cuda_stream)
-        _lib.check(rc)
+        state = self._state.data_ptr() if self._state is not None else None
+        if torch.cuda.current_device() == self._dev_index:
+            rc = self._push(r, state, p0, slab)
+        else:
+            with torch.cuda.device(self.device):
+                rc = self._push(r, state, p0, slab)
+        if rc:
+            _lib.check(rc)
         self._account(p0)
         self.rows_pushed += 1
+        self._state_rows = self.rows_pushed
         return slab
+
+    def _push(self, r, state, p0, slab) -> int:
+        stream = torch.cuda.current_stream().cuda_stream
+        if state is not None and self._state_rows < p0:
+            self._catch_up(p0, state, stream)
+        return self._lib.swdft2d_stream_push(
+            r.data_ptr(), _IN_CODES[r.dtype], self.N1, self._ring_ptr, state, self.m0, self.m1,
+            self.prec, self._factor, p0, slab.data_ptr() if slab is not None else None,
+            self._kernel_code, stream)
+
+    def _catch_up(self, p0: int, state: int, stream: int) -> None:
+        """Bring the level state up to row p0 - 1 after push_rows: replay the last
+        n0 - 1 rows from the raw ring (no output).  A level-l value the next pushes read
+        depends only on those rows, so the state's older content does not matter."""
+        code = _lib.IN_C128 if self.prec == _lib.PREC_FP64 else _lib.IN_C64
+        esz = self._ring.element_size()
+        for q in range(max(self._state_rows, p0 - self.n0 + 1), p0):
+            row = self._ring.data_ptr() + (q % self.n0) * self.N1 * esz
+            _lib.check(self._lib.swdft2d_stream_push(row, code, self.N1, None, state, self.m0,
+                                                     self.m1, self.prec, self._factor, q, None,
+                                                     self._kernel_code, stream))
+        self._state_rows = p0
 
     def push_rows(self, rows):
         """Ingest k rows at once (a [k, N1] block); returns the [k', P1, n0, n1] slabs

@@ -5,6 +5,7 @@ import hashlib
 
 import numpy as np
 import pytest
+import torch
 
 from conftest import sha
 from paper_1707_08213_b200 import ContainerError, OpCounter, WindowSpec
@@ -92,9 +93,13 @@ def test_container_from_device_tensor(golden, cuda, tmp_path):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("kernel", ["auto", "stream"])
 @pytest.mark.parametrize("shape,m", [((30, 20), (2, 2)), ((19, 33), (3, 1)), ((12, 12), (0, 3)),
-                                     ((70, 130), (6, 6)), ((7, 6), (0, 0))])
-def test_row_stream_equals_batch(cuda, oracle_lib, shape, m):
+                                     ((70, 130), (6, 6)), ((7, 6), (0, 0)), ((40, 9), (5, 0)),
+                                     ((22, 70), (1, 6))])
+def test_row_stream_equals_batch(cuda, oracle_lib, shape, m, kernel):
+    """kernel "auto": incremental K2 pushes over the level state; "stream": K1 re-run
+    over the raw ring per push.  Both bitwise equal to the batch rows (fp64)."""
     from paper_1707_08213_b200.stream import SlidingRowStream2D
 
     rng = np.random.default_rng(shape[0] * 7 + m[0])
@@ -102,7 +107,8 @@ def test_row_stream_equals_batch(cuda, oracle_lib, shape, m):
     n0, n1 = 1 << m[0], 1 << m[1]
     ref = oracle_lib.tree2d(x, *m)
     c = OpCounter(shape)
-    st = SlidingRowStream2D(WindowSpec(m), shape[1], counter=c)
+    st = SlidingRowStream2D(WindowSpec(m), shape[1], counter=c, kernel=kernel)
+    assert (st._state is not None) == (kernel == "auto")
     for p0 in range(shape[0]):
         slab = st.push_row(x[p0])
         if p0 < n0 - 1:
@@ -157,6 +163,51 @@ def test_row_stream_blocks_equal_batch(cuda, oracle_lib, shape, m):
     tail = [st2.push_row(x[i]) for i in range(3, shape[0])]
     n0 = 1 << m[0]
     assert np.array_equal(tail[-1].cpu().numpy().view(np.uint64), ref[-1].view(np.uint64))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+@pytest.mark.parametrize("shape,m", [((90, 75), (4, 3)), ((150, 70), (6, 6)), ((33, 17), (2, 4))])
+def test_row_stream_mixed_pushes(cuda, oracle_lib, shape, m, precision):
+    """Blocks and single pushes interleaved (the level state is re-derived from the raw
+    ring after each block), unitary normalization, real float32 rows: every slab equals
+    the batch row — bitwise in fp64, within 1e-4 of the window norm in fp32."""
+    from paper_1707_08213_b200.core import normalization_factor
+    from paper_1707_08213_b200.stream import SlidingRowStream2D
+
+    rng = np.random.default_rng(sum(shape) + m[0])
+    x = rng.standard_normal(shape).astype(np.float32)
+    spec = WindowSpec(m, "unitary")
+    n0 = 1 << m[0]
+    ref = oracle_lib.tree2d(x, *m, scale=normalization_factor(spec))
+    st = SlidingRowStream2D(spec, shape[1], precision=precision)
+    xd = torch.from_numpy(x).to(cuda)
+    got, r = {}, 0
+    plan = [1, 3, n0 + 2, 1, 1, 2, 5, n0 - 1 if n0 > 1 else 1, 1, 7, 1]
+    while r < shape[0]:
+        for k in plan:
+            k = min(k, shape[0] - r)
+            if k <= 0:
+                break
+            if k == 1 and r % 2 == 0:
+                slab = st.push_row(xd[r])
+                if slab is not None:
+                    got[r - n0 + 1] = slab.cpu().numpy()
+            else:
+                out = st.push_rows(xd[r:r + k])
+                if out is not None:
+                    first = max(0, r - n0 + 1)
+                    for i in range(out.shape[0]):
+                        got[first + i] = out[i].cpu().numpy()
+            r += k
+    assert sorted(got) == list(range(ref.shape[0]))
+    g = np.stack([got[i] for i in range(ref.shape[0])])
+    if precision == "fp64":
+        assert np.array_equal(g.view(np.uint64), ref.view(np.uint64))
+    else:
+        import oracle
+
+        assert oracle.window_rel_err(g, ref) <= 1e-4
 
 
 @pytest.mark.gpu
