@@ -364,13 +364,15 @@ const K1Info *k1_info() {
 // picked Q = 2 for m0 = 3..5 (c3 in fp64: 369 Gcoef/s at Q=2 vs 243 at Q=3; 8x8: 317
 // vs 292 at Q=1).
 struct K1Choice {
-    int m0, m1, q, tp1;
+    int m0, m1, q, tp1, minb = 1;  // minb: __launch_bounds__ min CTAs per SM (register cap)
 };
 constexpr K1Choice K1_TUNED_FP32[] = {
     {2, 3, 0, 32}, {3, 2, 0, 64}, {3, 4, 1, 2}, {4, 3, 2, 8}, {4, 6, 1, 1}, {5, 2, 3, 8},
     {5, 4, 3, 2},  {5, 6, 2, 1},  {6, 2, 3, 2}, {6, 3, 3, 2}, {6, 4, 3, 1}, {6, 5, 3, 1},
 };
-constexpr K1Choice K1_TUNED_FP64[] = {{3, 4, 1, 2}};
+// fp64 (4,4): MINB 4 caps registers at 128 (157 uncapped, 3 CTAs/SM, latency-bound):
+// +13 % on config 2, +4 % on config 4 in bitwise mode (profiles/TUNING_r01.md)
+constexpr K1Choice K1_TUNED_FP64[] = {{3, 4, 1, 2}, {4, 4, 2, 2, 4}};
 constexpr int k1_choose_q(int M0, int M1, bool DBL = false) {
     for (const K1Choice &c : K1_TUNED_FP32)
         if (!DBL && c.m0 == M0 && c.m1 == M1) return c.q;
@@ -391,14 +393,23 @@ constexpr int k1_choose_tp1(int M0, int M1, int Q, bool DBL = false) {
     return per >= 128 ? 1 : 128 / per;
 }
 
+constexpr int k1_choose_minb(int M0, int M1, bool DBL = false) {
+    for (const K1Choice &c : K1_TUNED_FP32)
+        if (!DBL && c.m0 == M0 && c.m1 == M1) return c.minb;
+    for (const K1Choice &c : K1_TUNED_FP64)
+        if (DBL && c.m0 == M0 && c.m1 == M1) return c.minb;
+    return 1;
+}
+
 template <int M0, int M1, bool DBL> struct K1Inst {
     using T = typename std::conditional<DBL, double, float>::type;
     static constexpr int Q = k1_choose_q(M0, M1, DBL);
     static constexpr int TP1 = k1_choose_tp1(M0, M1, Q, DBL);
+    static constexpr int MINB = k1_choose_minb(M0, M1, DBL);
     using S = K1Shape<M0, M1, Q, TP1>;
     static void reg() {
-        register_k1(k1_info<T, M0, M1, Q, TP1, DBL>());
-        register_k1(k1_info<T, M0, M1, Q, TP1, DBL, 1, 1, true>());
+        register_k1(k1_info<T, M0, M1, Q, TP1, DBL, MINB>());
+        register_k1(k1_info<T, M0, M1, Q, TP1, DBL, MINB, 1, true>());
     }
 };
 

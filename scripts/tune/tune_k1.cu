@@ -4,6 +4,7 @@
 #include "../../paper_1707_08213_b200/csrc/abi.cu"
 #include "../../paper_1707_08213_b200/csrc/k1_stream.cuh"
 #include "../../paper_1707_08213_b200/csrc/k0_window.cu"
+#include "../../paper_1707_08213_b200/csrc/k2_push.cu"
 
 namespace swdft2d {
 void k1_register_m0_0() {}
@@ -22,9 +23,9 @@ struct Variant { const char *name; const K1Info *(*info)(); };
     {"double m0=" #M0 " m1=" #M1 " Q=" #Q " TP1=" #TP1 " MINB=" #MINB,                  \
      &k1_info<double, M0, M1, Q, TP1, true, MINB, 1>}
 static const Variant VARIANTS[] = {
-    V(float, 4, 4, 2, 2, 1, 1), V(float, 4, 4, 2, 1, 1, 1), V(float, 4, 4, 1, 2, 1, 1),
-    V(float, 4, 4, 3, 1, 1, 1), V(float, 4, 4, 2, 4, 1, 1), V(float, 4, 4, 2, 1, 2, 1),
-    V(float, 4, 4, 2, 2, 1, 2),
+    V64(4, 4, 2, 2, 1), V64(4, 4, 2, 2, 4), V64(4, 4, 2, 2, 5), V64(4, 4, 2, 2, 6),
+    V64(4, 4, 2, 1, 4), V64(4, 4, 2, 1, 8), V64(4, 4, 1, 4, 4),
+    V64(5, 3, 2, 4, 1), V64(5, 3, 2, 4, 3), V64(5, 3, 2, 4, 4), V64(5, 3, 2, 2, 6),
 };
 }  // namespace swdft2d
 
