@@ -269,10 +269,13 @@ def run_ours(args, cfg, rank, world, local_rank):
     times = []
     with ClockSampler(local_rank) as clk:
         for _ in range(args.steps):
-            flush_l2(flush)
             if world > 1:
                 dist.barrier()
             torch.cuda.synchronize()
+            # the L2 flush is queued just ahead of the start event, so the device is still
+            # busy with it while the step is submitted: the events time the step's device
+            # work, not the host's submission latency
+            flush_l2(flush)
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
@@ -311,8 +314,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         "config": {"workload": cfg.name, "desc": cfg.desc, "N0": cfg.N0, "N1": cfg.N1,
                    "window": [n0, n1], "coefficients": cfg.coefficients,
                    "output_bytes": cfg.coefficients * out_bpc,
-                   "l2": "256 MiB flush write between timed steps (outside the events); "
-                         "output >> L2 as well",
+                   "l2": "256 MiB flush write before every timed step (queued ahead of the "
+                         "start event, outside the timed interval); output >> L2 as well",
                    "parallelism": (f"strips{world} (NCCL scatter from rank 0)" if strips else
                                    f"replicas{world} (each rank its own full workload, no "
                                    "data-path collective)" if world > 1 else "single"),
@@ -381,8 +384,8 @@ def other_configs(args, main_cfg, dev, flush, stream):
         g.replay()
         ts = []
         for _ in range(5):
-            flush_l2(flush)
             torch.cuda.synchronize()
+            flush_l2(flush)  # ahead of the start event (see run_ours)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
             g.replay()
