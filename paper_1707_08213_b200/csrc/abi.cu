@@ -348,13 +348,42 @@ int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t
                     (long long)p0_begin, (long long)p0_end, (long long)P0);
     if (p0_begin == p0_end) return SWDFT2D_OK;
     if (!x || !out) return fail(SWDFT2D_E_INVALID_ARG, "null device pointer");
-    if (kernel < SWDFT2D_KERNEL_AUTO || kernel > SWDFT2D_KERNEL_STREAM_TMA)
+    if (kernel < SWDFT2D_KERNEL_AUTO || kernel > SWDFT2D_KERNEL_ROWS)
         return fail(SWDFT2D_E_INVALID_ARG, "unknown kernel code %d", kernel);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     DeviceState *ds = nullptr;
     if ((rc = device_state(&ds))) return rc;
     const int n0 = 1 << m0;
     const bool apply = !(scale == 1.0);
+
+    if (kernel == SWDFT2D_KERNEL_ROWS && m0 != 0)
+        return fail(SWDFT2D_E_UNSUPPORTED, "the row-tree kernel needs n0 = 1 (m0 = %d)", m0);
+    if ((kernel == SWDFT2D_KERNEL_ROWS || kernel == SWDFT2D_KERNEL_AUTO) && m0 == 0) {
+        if (m1 > SWDFT2D_K0_MAX_M)
+            return fail(SWDFT2D_E_UNSUPPORTED, "window 1 x 2^%d exceeds the CUDA paths (max 2^%d)",
+                        m1, SWDFT2D_K0_MAX_M);
+        const void *tw64 = nullptr, *tw32 = nullptr;
+        if ((rc = k0_tables(ds, &tw64, &tw32))) return rc;
+        KRParams P;
+        std::memset(&P, 0, sizeof P);
+        P.x = x;
+        P.in_dtype = in_dtype;
+        P.apply_scale = apply ? 1 : 0;
+        P.N1 = N1;
+        P.ldx = ld_x;
+        P.p0_begin = p0_begin;
+        P.p0_end = p0_end;
+        P.P1 = P1;
+        P.out = out;
+        P.scale = scale;
+        P.tw = prec == SWDFT2D_PREC_FP64 ? tw64 : tw32;
+        P.sms = ds->sms;
+        const int r = launch_kr(P, m1, prec, st);
+        if (r != 0) return fail(SWDFT2D_E_CUDA, "row-tree kernel launch setup failed (%d)", r);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return fail(SWDFT2D_E_CUDA, "kernel launch: %s", cudaGetErrorString(e));
+        return SWDFT2D_OK;
+    }
 
     const K1Info *k1 = find_k1(m0, m1, prec, 0);
     if ((kernel == SWDFT2D_KERNEL_STREAM || kernel == SWDFT2D_KERNEL_STREAM_TMA) && !k1)
@@ -542,7 +571,7 @@ int swdft2d_stream_push(const void *row, int in_dtype, int64_t N1, void *ring, v
         return fail(SWDFT2D_E_INVALID_ARG, "unknown input dtype code %d", in_dtype);
     if (prec != SWDFT2D_PREC_FP32 && prec != SWDFT2D_PREC_FP64)
         return fail(SWDFT2D_E_INVALID_ARG, "unknown precision code %d", prec);
-    if (kernel < SWDFT2D_KERNEL_AUTO || kernel > SWDFT2D_KERNEL_STREAM_TMA)
+    if (kernel < SWDFT2D_KERNEL_AUTO || kernel > SWDFT2D_KERNEL_ROWS)
         return fail(SWDFT2D_E_INVALID_ARG, "unknown kernel code %d", kernel);
     if (p0 < 0) return fail(SWDFT2D_E_INVALID_ARG, "negative row index %lld", (long long)p0);
     if (m0 < 0 || m1 < 0 || m0 > 30) return fail(SWDFT2D_E_INVALID_WINDOW, "bad window exponents");

@@ -51,6 +51,20 @@ void register_k1(const K1Info *info);
 
 int launch_k0(const K0Params &P, int prec, cudaStream_t stream);
 
+// KR: row-tree kernel for n0 = 1 windows (kr_rows.cu), n1 up to 1024.
+struct KRParams {
+    const void *x;
+    int in_dtype, apply_scale;
+    int64_t N1, ldx;
+    int64_t p0_begin, p0_end, P1;
+    void *out;
+    double scale;
+    const void *tw;  // device make_twiddles(K0_TW_N) of the precision (float2 / double2)
+    int sms;         // SMs of the device (persistent grid = SMs x occupancy)
+};
+// 0 ok, -2 shared-memory attribute / occupancy refused, -3 m1 out of range
+int launch_kr(const KRParams &P, int m1, int prec, cudaStream_t stream);
+
 // K2: one incremental stream push (k2_push.cu).
 struct K2Params {
     const void *row;  // the pushed row, N1 elements of in_dtype

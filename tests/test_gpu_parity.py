@@ -378,6 +378,53 @@ def test_large_windows_k0_and_unsupported(cuda, oracle_lib):
         run(y, 11, 0, "fp64")                                     # beyond K0's 2^10
 
 
+@pytest.mark.parametrize("m1", list(range(0, 11)))
+def test_row_kernel_windows(cuda, oracle_lib, m1):
+    """KR (n0 = 1 windows, n1 = 1 .. 1024): bitwise vs the oracle in fp64 on a strided
+    complex input with a ragged last tile, equal to K1 bitwise where K1 exists (n1 <= 64),
+    window-row ranges, fp32 within tolerance, unitary scale fused."""
+    rng = np.random.default_rng(100 + m1)
+    n1 = 1 << m1
+    N0, N1 = 3, n1 + 37 + (m1 * 13) % 29
+    x = rng.standard_normal((N0, N1)) + 1j * rng.standard_normal((N0, N1))
+    ref = oracle_lib.tree2d(x, 0, m1)
+    got = run(x, 0, m1, "fp64")                               # auto -> KR
+    assert bits_equal(got, ref)
+    assert bits_equal(run(x, 0, m1, "fp64", kernel="rows"), ref)
+    if m1 <= 6:
+        assert bits_equal(run(x, 0, m1, "fp64", kernel="stream"), ref)
+    assert rel_err(run(x.astype(np.complex64), 0, m1, "fp32"), ref) <= FP32_TOL
+    # strided rows (ld_x > N1) and a window-row range, through the ABI directly
+    wide = torch.zeros((N0, N1 + 5), dtype=torch.complex128, device=cuda)
+    wide[:, :N1] = torch.from_numpy(x).to(cuda)
+    P1 = N1 - n1 + 1
+    part = torch.empty((2, P1, 1, n1), dtype=torch.complex128, device=cuda)
+    forward_into(wide[:, :N1], 0, m1, part, prec=_lib.PREC_FP64, p0_begin=1, p0_end=3,
+                 kernel="rows")
+    assert bits_equal(part.cpu().numpy(), ref[1:3])
+    from paper_1707_08213_b200.core import normalization_factor
+
+    spec = WindowSpec((0, m1), "unitary")
+    refu = oracle_lib.tree2d(x, 0, m1, scale=normalization_factor(spec))
+    assert bits_equal(run(x, 0, m1, "fp64", normalization="unitary"), refu)
+
+
+def test_row_kernel_1d_large_and_errors(cuda, oracle_lib):
+    """tree_swdft_1d with windows up to 1024 runs on KR (bitwise); kernel="rows" with
+    n0 > 1 fails loudly."""
+    from paper_1707_08213_b200 import UnsupportedError
+    from paper_1707_08213_b200.tree1d import tree_swdft_1d
+
+    rng = np.random.default_rng(21)
+    s = rng.standard_normal(3000)
+    for m in (7, 9, 10):
+        ref = oracle_lib.tree2d(s.reshape(1, -1), 0, m)[0, :, 0, :]
+        got = tree_swdft_1d(s, WindowSpec((m,))).values.cpu().numpy()
+        assert bits_equal(got, ref)
+    with pytest.raises(UnsupportedError):
+        run(rng.standard_normal((10, 10)), 1, 2, "fp64", kernel="rows")
+
+
 def test_host_output_pipeline(cuda, oracle_lib):
     """to_host / host_out: strips computed in a device ring and streamed to pinned host
     memory equal the device-resident result bit for bit (fp64), with many strips."""
