@@ -322,7 +322,11 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
                             constexpr int u = decltype(uc)::value;
                             C val = cur[u];
                             if (P.apply_scale) val = cscale(val, (T)P.scale);
+#ifdef K1_PLAIN_STORES  // tuning builds: default-policy stores instead of evict-first
+                            o[(j + J * u) * n1] = val;
+#else
                             st_stream(o + (j + J * u) * n1, val);
+#endif
                         });
                     }
                 });

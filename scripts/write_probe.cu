@@ -4,6 +4,9 @@
 //   chunked     : each CTA streams its own contiguous region
 //   k1pattern   : each CTA writes 32 KB blocks at a 33 MB stride (K1's C4 output pattern)
 //   memset      : cudaMemsetAsync
+//   gs256cs / gs256 : grid-stride 32-byte stores (st.global[.cs].v8.f32, Blackwell STG.256)
+//   gs8cs       : grid-stride 8-byte streaming stores (K1's float2 store width)
+//   gszero      : grid-stride 16-byte streaming stores of zeros (compressible data)
 // Values are per-thread varying (not compressible) unless noted.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o write_probe write_probe.cu
 #include <cstdio>
@@ -17,6 +20,26 @@ __global__ void chunked(float4 *p, size_t n) {
     size_t per = (n + gridDim.x - 1) / gridDim.x, b = blockIdx.x * per, e = b + per < n ? b + per : n;
     for (size_t i = b + threadIdx.x; i < e; i += blockDim.x)
         __stcs(p + i, make_float4((float)i, 1.f, 2.f, (float)threadIdx.x));
+}
+template <bool CS>
+__global__ void gridstride256(float4 *p, size_t n) {  // n float4 = n / 2 32-byte units
+    size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x, st = (size_t)gridDim.x * blockDim.x;
+    for (; i < n / 2; i += st) {
+        float *q = reinterpret_cast<float *>(p + 2 * i);
+        const float a = (float)i, b = (float)threadIdx.x;
+        if (CS)
+            asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%1,%2,%1,%2,%1,%2};" :: "l"(q), "f"(a), "f"(b) : "memory");
+        else
+            asm volatile("st.global.v8.f32 [%0], {%1,%2,%1,%2,%1,%2,%1,%2};" :: "l"(q), "f"(a), "f"(b) : "memory");
+    }
+}
+__global__ void gridstride8(float2 *p, size_t n) {  // n float2
+    size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x, st = (size_t)gridDim.x * blockDim.x;
+    for (; i < n; i += st) __stcs(p + i, make_float2((float)i, (float)threadIdx.x));
+}
+__global__ void gridstridezero(float4 *p, size_t n) {
+    size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x, st = (size_t)gridDim.x * blockDim.x;
+    for (; i < n; i += st) __stcs(p + i, make_float4(0.f, 0.f, 0.f, 0.f));
 }
 // block of 2048 float4 (32 KB) per "row"; rows of a CTA are `stride` float4 apart
 __global__ void k1pattern(float4 *p, size_t n, size_t stride, size_t nblk_per_row) {
@@ -86,7 +109,7 @@ int main() {
             printf("{\"mode\": \"bulkstore16K\", \"ctas_per_sm\": %d, \"GBps\": %.1f}\n", occ * 2, bytes / best2 / 1e6);
         }
     }
-    for (int mode = 0; mode < 4; ++mode)
+    for (int mode = 0; mode < 8; ++mode)
         for (int occ : {2, 4, 8}) {
             float best = 1e30f;
             size_t written = bytes;
@@ -95,13 +118,18 @@ int main() {
                 if (mode == 0) gridstride<<<sms * occ, 512>>>(p, n);
                 else if (mode == 1) chunked<<<sms * occ, 512>>>(p, n);
                 else if (mode == 2) k1pattern<<<sms * occ, 512>>>(p, n, stride, nblk);
-                else cudaMemsetAsync(p, rep + 1, bytes);
+                else if (mode == 3) cudaMemsetAsync(p, rep + 1, bytes);
+                else if (mode == 4) gridstride256<true><<<sms * occ, 512>>>(p, n);
+                else if (mode == 5) gridstride256<false><<<sms * occ, 512>>>(p, n);
+                else if (mode == 6) gridstride8<<<sms * occ, 512>>>(reinterpret_cast<float2 *>(p), 2 * n);
+                else gridstridezero<<<sms * occ, 512>>>(p, n);
                 cudaEventRecord(b); cudaEventSynchronize(b);
                 float ms; cudaEventElapsedTime(&ms, a, b);
                 if (ms < best) best = ms;
             }
             if (mode == 2) written = (n / stride) * stride * 16;
-            const char *nm[] = {"gridstride", "chunked", "k1pattern", "memset"};
+            const char *nm[] = {"gridstride", "chunked", "k1pattern", "memset",
+                                "gs256cs", "gs256", "gs8cs", "gszero"};
             printf("{\"mode\": \"%s\", \"ctas_per_sm\": %d, \"GBps\": %.1f}\n", nm[mode], occ,
                    written / best / 1e6);
             if (mode == 3) break;
