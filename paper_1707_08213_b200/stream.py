@@ -236,10 +236,12 @@ class SlidingRowStream2D:
 
 
 class SlidingStream1D:
-    """Sample-push 1D stream (tree1d.py:63-119 interface) on the GPU: a device ring of
-    the last n samples (double-stored, so the window is one contiguous view); every push
-    with p >= n - 1 returns the n-point transform of the last n samples (K1 with
-    m0 = 0 over a 1 x n row), bitwise equal to the batch 1D tree in fp64."""
+    """Sample-push 1D stream (tree1d.py:63-119 interface) on the GPU.  For n <= 64 every
+    push is one K2 launch over the tree's level state (the 1D tree is the dim-0 tree of a
+    one-column 2D stream); larger windows keep a device ring of the last n samples
+    (double-stored, so the window is one contiguous view) and run KR over it.  Once
+    p >= n - 1 a push returns the n-point transform of the last n samples, bitwise equal
+    to the batch 1D tree in fp64."""
 
     def __init__(self, spec, counter=None, *, precision="fp64", device=None):
         if len(spec.exponents) != 1:
@@ -251,8 +253,19 @@ class SlidingStream1D:
         self.prec = _precision_code(precision, None)
         self.device = torch.device(device) if device is not None else torch.device(
             "cuda", torch.cuda.current_device())
-        self._factor = core.normalization_factor(spec)
+        self._factor = float(core.normalization_factor(spec))
         self._ring = torch.zeros(2 * self.n, dtype=_RING_DTYPES[self.prec], device=self.device)
+        # n <= 64: K2 pushes (the 1D tree is the dim-0 tree of a 1-column 2D stream:
+        # m0 = m, m1 = 0, N1 = 1), one launch per sample over the level state
+        self._state = None
+        if self.m <= _lib.K1_MAX_M:
+            self._lib = _lib.load()
+            nbytes = ctypes.c_int64()
+            _lib.check(self._lib.swdft2d_stream_state_bytes(1, self.m, 0, self.prec,
+                                                            ctypes.byref(nbytes)))
+            self._state = torch.zeros(max(1, nbytes.value), dtype=torch.uint8, device=self.device)
+            self._sample = torch.zeros(1, dtype=_RING_DTYPES[self.prec], device=self.device)
+            self._code = _lib.IN_C128 if self.prec == _lib.PREC_FP64 else _lib.IN_C64
         self.pushed = 0
         self.ops_last_push = 0
         self.closed = False
@@ -264,10 +277,11 @@ class SlidingStream1D:
             raise core.StateError("push after close")
         p = self.pushed
         n = self.n
-        slot = p % n
         v = complex(sample) if not isinstance(sample, torch.Tensor) else sample
-        self._ring[slot] = v
-        self._ring[slot + n] = v
+        if self._state is None:
+            slot = p % n
+            self._ring[slot] = v
+            self._ring[slot + n] = v
         ops = 0
         for l in range(1, self.m + 1):  # tree1d.py:101-108
             s = 1 << (self.m - l)
@@ -278,6 +292,17 @@ class SlidingStream1D:
                 self.counter.add_region((p,), 1 << l, 1)
         self.ops_last_push = ops
         self.pushed += 1
+        if self._state is not None:
+            self._sample.fill_(v) if not isinstance(v, torch.Tensor) else self._sample.copy_(
+                v.reshape(1))
+            out = torch.empty(n, dtype=_OUT_DTYPES[self.prec], device=self.device) \
+                if p >= n - 1 else None
+            with torch.cuda.device(self.device):
+                _lib.check(self._lib.swdft2d_stream_push(
+                    self._sample.data_ptr(), self._code, 1, None, self._state.data_ptr(), self.m,
+                    0, self.prec, self._factor, p, out.data_ptr() if out is not None else None,
+                    _lib.KERNEL_AUTO, torch.cuda.current_stream(self.device).cuda_stream))
+            return out
         if p < n - 1:
             return None
         first = (p + 1) % n

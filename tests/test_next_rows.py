@@ -327,3 +327,24 @@ def test_stream1d_matches_reference(golden, cuda):
             outs.append(r.cpu().numpy())
     assert sha(np.stack(outs)) == rec["sha"]
     assert ops == rec["ops"] and c.total == rec["total"] and sha(c.position_ops) == rec["pos_sha"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m", [0, 1, 4, 6, 8])
+def test_stream1d_equals_batch(cuda, m):
+    """Sample pushes (K2 for n <= 64, the ring + KR above) emit the batch 1D tree's
+    rows bitwise (fp64), with the unitary scale."""
+    from paper_1707_08213_b200.stream import SlidingStream1D
+    from paper_1707_08213_b200.tree1d import tree_swdft_1d
+
+    rng = np.random.default_rng(70 + m)
+    n = 1 << m
+    sig = rng.standard_normal(n + 37) + 1j * rng.standard_normal(n + 37)
+    spec = WindowSpec((m,), "unitary")
+    ref = tree_swdft_1d(sig, spec).values.cpu().numpy()
+    st = SlidingStream1D(spec)
+    assert (st._state is not None) == (m <= 6)
+    got = [st.push(v) for v in sig]
+    assert all(g is None for g in got[:n - 1])
+    g = np.stack([x.cpu().numpy() for x in got[n - 1:]])
+    assert np.array_equal(g.view(np.uint64), ref.view(np.uint64))
