@@ -100,3 +100,46 @@ def test_special_values_fp64(cuda, oracle_lib):
             rn, gn = np.isnan(ref.view(np.float64)), np.isnan(got.view(np.float64))
             assert np.array_equal(rn, gn)
             assert np.array_equal(ref.view(np.uint64)[~rn], got.view(np.uint64)[~gn])
+
+
+@settings(max_examples=40, deadline=None, suppress_health_check=list(HealthCheck))
+@given(N0=st.integers(1, 3), m1=st.integers(0, 10), extra=st.integers(0, 700),
+       cplx=st.booleans(), seed=st.integers(0, 2**31 - 1))
+def test_fuzz_row_kernel_fp64_bitwise(cuda, oracle_lib, N0, m1, extra, cplx, seed):
+    """KR (n0 = 1, n1 up to 1024) on random widths, ragged tiles included."""
+    N1 = (1 << m1) + extra
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((N0, N1)) + (1j * rng.standard_normal((N0, N1)) if cplx else 0)
+    ref = oracle_lib.tree2d(x, 0, m1)
+    got = run(x, (0, m1), kernel="rows")
+    assert np.array_equal(got.view(np.uint64), ref.view(np.uint64))
+
+
+@settings(max_examples=25, deadline=None, suppress_health_check=list(HealthCheck))
+@given(N0=st.integers(1, 30), N1=st.integers(1, 50), m0=st.integers(0, 5), m1=st.integers(0, 5),
+       blocks=st.lists(st.integers(1, 9), min_size=1, max_size=12), seed=st.integers(0, 2**31 - 1))
+def test_fuzz_row_stream_fp64_bitwise(cuda, oracle_lib, N0, N1, m0, m1, blocks, seed):
+    """Row-push stream (K2 single pushes, K1 blocks, state catch-up) == batch rows."""
+    from paper_1707_08213_b200.stream import SlidingRowStream2D
+
+    if (1 << m0) > N0 or (1 << m1) > N1:
+        return
+    rng = np.random.default_rng(seed)
+    x = rng.standard_normal((N0, N1)) + 1j * rng.standard_normal((N0, N1))
+    ref = oracle_lib.tree2d(x, m0, m1)
+    st_ = SlidingRowStream2D(WindowSpec((m0, m1)), N1)
+    n0, got, r, i = 1 << m0, [], 0, 0
+    while r < N0:
+        k = min(blocks[i % len(blocks)], N0 - r)
+        i += 1
+        if k == 1:
+            s = st_.push_row(x[r])
+            if s is not None:
+                got.append(s.cpu().numpy()[None])
+        else:
+            o = st_.push_rows(x[r:r + k])
+            if o is not None:
+                got.append(o.cpu().numpy())
+        r += k
+    g = np.concatenate(got)
+    assert np.array_equal(g.view(np.uint64), ref.view(np.uint64))
