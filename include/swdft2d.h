@@ -60,13 +60,14 @@ extern "C" {
 #define SWDFT2D_PREC_FP64 1 /* complex128 out */
 
 /* kernel selection for swdft2d_forward */
-#define SWDFT2D_KERNEL_AUTO 0       /* KR if n0 = 1, else K1 when instantiated, else K0   */
+#define SWDFT2D_KERNEL_AUTO 0       /* KR if n0 = 1, else K1 (n <= 64), else KR + KC       */
 #define SWDFT2D_KERNEL_STREAM 1     /* K1, input by register prefetch (LDG)               */
 #define SWDFT2D_KERNEL_WINDOW 2     /* K0: per-(window, k1) DAG kernel (bring-up)          */
 #define SWDFT2D_KERNEL_STREAM_TMA 3 /* K1, input tiles staged by TMA when x is addressable */
 #define SWDFT2D_KERNEL_ROWS 4       /* KR: row-tree kernel, windows with n0 = 1 (1D), n1 <= 1024 */
+#define SWDFT2D_KERNEL_SEPARABLE 5  /* KR (rows) + KC (columns) over a workspace, any n <= 1024 */
 
-/* Largest window exponent handled by K1 / by K0 and KR. */
+/* Largest window exponent handled by K1 / by K0, KR and KR + KC. */
 #define SWDFT2D_K1_MAX_M 6
 #define SWDFT2D_K0_MAX_M 10
 

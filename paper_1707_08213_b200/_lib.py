@@ -29,8 +29,9 @@ IN_F32, IN_F64, IN_C64, IN_C128 = 0, 1, 2, 3
 K1_MAX_M, K0_MAX_M = 6, 10  # SWDFT2D_K1_MAX_M / SWDFT2D_K0_MAX_M
 PREC_FP32, PREC_FP64 = 0, 1
 KERNEL_AUTO, KERNEL_STREAM, KERNEL_WINDOW, KERNEL_STREAM_TMA, KERNEL_ROWS = 0, 1, 2, 3, 4
+KERNEL_SEPARABLE = 5
 KERNELS = {"auto": KERNEL_AUTO, "stream": KERNEL_STREAM, "window": KERNEL_WINDOW,
-           "stream_tma": KERNEL_STREAM_TMA, "rows": KERNEL_ROWS}
+           "stream_tma": KERNEL_STREAM_TMA, "rows": KERNEL_ROWS, "separable": KERNEL_SEPARABLE}
 
 # every symbol include/swdft2d.h declares: name -> (restype, argtypes)
 _i64, _int, _dbl, _vp = ctypes.c_int64, ctypes.c_int, ctypes.c_double, ctypes.c_void_p

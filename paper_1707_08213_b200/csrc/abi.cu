@@ -248,6 +248,65 @@ static int64_t k1_rows_per_tile(int64_t rows, int64_t CB, int64_t slots, int n0)
     return best_rch;
 }
 
+// Large-window path (n0 or n1 above K1's 2^6, up to 2^10): the separable schedule in
+// strips of window rows — KR writes the strip's stage-R rows Z (the dim-1 tree of each
+// input row, unscaled) into a stream-ordered workspace, KC runs the dim-0 trees down
+// Z's columns into the output.  Workspace <= ~512 MB per call (cudaMallocAsync /
+// cudaFreeAsync on the caller's stream, so concurrent streams never share it).
+static int forward_separable(const void *x, int in_dtype, int64_t N1, int64_t ld_x, int m0,
+                             int m1, int prec, double scale, int64_t p0_begin, int64_t p0_end,
+                             void *out, cudaStream_t st, DeviceState *ds, const void *tw) {
+    const int64_t n0 = (int64_t)1 << m0, n1 = (int64_t)1 << m1;
+    const int64_t P1 = N1 - n1 + 1, cols = P1 * n1;
+    const int64_t esz = prec == SWDFT2D_PREC_FP64 ? 16 : 8;
+    const int64_t rows = p0_end - p0_begin;
+    const int64_t zrow = cols * esz;
+    int64_t R = ((int64_t)512 << 20) / zrow - (n0 - 1);
+    if (R < 64) R = 64;
+    if (R > rows) R = rows;
+    void *z = nullptr;
+    cudaError_t e = cudaMallocAsync(&z, (size_t)((R + n0 - 1) * zrow), st);
+    if (e != cudaSuccess)
+        return fail(SWDFT2D_E_NOMEM, "large-window workspace (%lld B): %s",
+                    (long long)((R + n0 - 1) * zrow), cudaGetErrorString(e));
+    int rc = SWDFT2D_OK;
+    for (int64_t a = p0_begin; a < p0_end && rc == SWDFT2D_OK; a += R) {
+        const int64_t b = a + R < p0_end ? a + R : p0_end;
+        KRParams r;
+        std::memset(&r, 0, sizeof r);
+        r.x = x;
+        r.in_dtype = in_dtype;
+        r.N1 = N1;
+        r.ldx = ld_x;
+        r.p0_begin = a;
+        r.p0_end = b + n0 - 1;  // input rows of the strip
+        r.P1 = P1;
+        r.out = z;
+        r.scale = 1.0;
+        r.tw = tw;
+        r.sms = ds->sms;
+        KCParams c;
+        std::memset(&c, 0, sizeof c);
+        c.z = z;
+        c.cols = cols;
+        c.zrows = b - a + n0 - 1;
+        c.P0s = b - a;
+        c.P1 = P1;
+        c.m1 = m1;
+        c.apply_scale = scale == 1.0 ? 0 : 1;
+        c.scale = scale;
+        c.out = static_cast<char *>(out) + (a - p0_begin) * P1 * n0 * n1 * esz;
+        c.tw = tw;
+        c.sms = ds->sms;
+        if (launch_kr(r, m1, prec, st) || launch_kc(c, m0, prec, st))
+            rc = fail(SWDFT2D_E_CUDA, "large-window launch setup failed (m0=%d m1=%d)", m0, m1);
+        else if ((e = cudaGetLastError()) != cudaSuccess)
+            rc = fail(SWDFT2D_E_CUDA, "large-window kernel launch: %s", cudaGetErrorString(e));
+    }
+    cudaFreeAsync(z, st);
+    return rc;
+}
+
 }  // namespace swdft2d
 
 using namespace swdft2d;
@@ -348,7 +407,7 @@ int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t
                     (long long)p0_begin, (long long)p0_end, (long long)P0);
     if (p0_begin == p0_end) return SWDFT2D_OK;
     if (!x || !out) return fail(SWDFT2D_E_INVALID_ARG, "null device pointer");
-    if (kernel < SWDFT2D_KERNEL_AUTO || kernel > SWDFT2D_KERNEL_ROWS)
+    if (kernel < SWDFT2D_KERNEL_AUTO || kernel > SWDFT2D_KERNEL_SEPARABLE)
         return fail(SWDFT2D_E_INVALID_ARG, "unknown kernel code %d", kernel);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     DeviceState *ds = nullptr;
@@ -358,7 +417,7 @@ int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t
 
     if (kernel == SWDFT2D_KERNEL_ROWS && m0 != 0)
         return fail(SWDFT2D_E_UNSUPPORTED, "the row-tree kernel needs n0 = 1 (m0 = %d)", m0);
-    if ((kernel == SWDFT2D_KERNEL_ROWS || kernel == SWDFT2D_KERNEL_AUTO) && m0 == 0) {
+    if ((kernel == SWDFT2D_KERNEL_ROWS || kernel == SWDFT2D_KERNEL_AUTO || kernel == SWDFT2D_KERNEL_SEPARABLE) && m0 == 0) {
         if (m1 > SWDFT2D_K0_MAX_M)
             return fail(SWDFT2D_E_UNSUPPORTED, "window 1 x 2^%d exceeds the CUDA paths (max 2^%d)",
                         m1, SWDFT2D_K0_MAX_M);
@@ -388,6 +447,15 @@ int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t
     const K1Info *k1 = find_k1(m0, m1, prec, 0);
     if ((kernel == SWDFT2D_KERNEL_STREAM || kernel == SWDFT2D_KERNEL_STREAM_TMA) && !k1)
         return fail(SWDFT2D_E_UNSUPPORTED, "no K1 instantiation for m0=%d m1=%d prec=%d", m0, m1, prec);
+    if (kernel == SWDFT2D_KERNEL_SEPARABLE || (kernel == SWDFT2D_KERNEL_AUTO && !k1)) {
+        if (m0 > SWDFT2D_K0_MAX_M || m1 > SWDFT2D_K0_MAX_M)
+            return fail(SWDFT2D_E_UNSUPPORTED, "window 2^%d x 2^%d exceeds the CUDA paths (max 2^%d)",
+                        m0, m1, SWDFT2D_K0_MAX_M);
+        const void *tw64 = nullptr, *tw32 = nullptr;
+        if ((rc = k0_tables(ds, &tw64, &tw32))) return rc;
+        return forward_separable(x, in_dtype, N1, ld_x, m0, m1, prec, scale, p0_begin, p0_end, out,
+                                 st, ds, prec == SWDFT2D_PREC_FP64 ? tw64 : tw32);
+    }
     if (kernel != SWDFT2D_KERNEL_WINDOW && k1) {
         K1Params P;
         std::memset(&P, 0, sizeof P);
@@ -571,7 +639,7 @@ int swdft2d_stream_push(const void *row, int in_dtype, int64_t N1, void *ring, v
         return fail(SWDFT2D_E_INVALID_ARG, "unknown input dtype code %d", in_dtype);
     if (prec != SWDFT2D_PREC_FP32 && prec != SWDFT2D_PREC_FP64)
         return fail(SWDFT2D_E_INVALID_ARG, "unknown precision code %d", prec);
-    if (kernel < SWDFT2D_KERNEL_AUTO || kernel > SWDFT2D_KERNEL_ROWS)
+    if (kernel < SWDFT2D_KERNEL_AUTO || kernel > SWDFT2D_KERNEL_SEPARABLE)
         return fail(SWDFT2D_E_INVALID_ARG, "unknown kernel code %d", kernel);
     if (p0 < 0) return fail(SWDFT2D_E_INVALID_ARG, "negative row index %lld", (long long)p0);
     if (m0 < 0 || m1 < 0 || m0 > 30) return fail(SWDFT2D_E_INVALID_WINDOW, "bad window exponents");

@@ -1,0 +1,219 @@
+// KC — column-tree kernel of the large-window path (windows with n0 > 64 or n1 > 64,
+// up to 1024 x 1024), the stage-C half of the separable schedule:
+//   stage R: KR writes Z[r][p1][k1], the dim-1 tree of every input row of a strip
+//            (row_level_step, tree2d.py:72-93) into a stream-ordered workspace;
+//   stage C: KC runs the dim-0 tree (col_level_step, tree2d.py:96-120) down every
+//            column c = (p1, k1) of Z and writes out[p0][p1][k0][k1].
+// The factorisation is exact, so fp64 stays bitwise.
+// KC is KR's shared-memory level schedule (radix-4 passes, the middle level in
+// registers; one radix-2 pass first when m0 is odd) with a column dimension: a CTA
+// owns CW consecutive columns (the fast index, so Z reads and output writes are
+// CW-element runs) x TP0 window rows.
+#include "swdft2d_device.cuh"
+#include "swdft2d_internal.h"
+
+namespace swdft2d {
+
+constexpr int KC_THREADS = 256;
+constexpr size_t KC_SMEM_CAP = 100 * 1024;
+
+// nodes of level t for TP0 window rows: (TP0 + s_t - 1) 2^t, per column
+__host__ __device__ constexpr int64_t kc_level_nodes(int M0, int TP0, int t) {
+    return (int64_t)(TP0 + (1 << (M0 - t)) - 1) << t;
+}
+// levels stored in shared memory (pass order t = 0, [1 if m0 odd], then every second up
+// to m0 - 2), alternating between buffers A (which = 0) and B (which = 1)
+__host__ __device__ constexpr int64_t kc_buf(int M0, int TP0, int which) {
+    int64_t best = 1;
+    int idx = 0;
+    for (int t = 0; t <= (M0 > 1 ? M0 - 2 : 0); ++t) {
+        const bool stored = t == 0 || (t % 2) == (M0 % 2);
+        if (!stored) continue;
+        const int64_t v = kc_level_nodes(M0, TP0, t);
+        if ((idx & 1) == which && v > best) best = v;
+        ++idx;
+    }
+    return best;
+}
+__host__ __device__ constexpr size_t kc_smem(int M0, int TP0, int CW, int esz) {
+    return (size_t)esz * ((size_t)CW * (kc_buf(M0, TP0, 0) + kc_buf(M0, TP0, 1)) + (1u << M0));
+}
+// tile shape: the widest column group (then the most window rows) within the cap
+template <typename T, int M0> struct KCShape {
+    static constexpr int pick(int what) {
+        const int cws[5] = {32, 16, 8, 4, 2};
+        const int tps[3] = {16, 8, 4};
+        for (int a = 0; a < 5; ++a)
+            for (int b = 0; b < 3; ++b)
+                if (kc_smem(M0, tps[b], cws[a], (int)sizeof(T) * 2) <= KC_SMEM_CAP)
+                    return what == 0 ? cws[a] : tps[b];
+        return what == 0 ? 1 : 1;
+    }
+    static constexpr int CW = pick(0), TP0 = pick(1);
+    static constexpr size_t SMEM = kc_smem(M0, TP0, CW, (int)sizeof(T) * 2);
+};
+
+template <typename T, bool EXACT, int M0, int TP0, int CW, int t, bool LAST>
+__device__ __forceinline__ void kc_pass4(const cplx<T> *src, cplx<T> *dst, const cplx<T> *stw,
+                                         int npos, int ncol, const KCParams &P, int64_t r0,
+                                         int64_t c0) {
+    using C = cplx<T>;
+    constexpr int n0 = 1 << M0, Lt = 1 << t, s2 = n0 >> (t + 2);
+    constexpr int cnt = LAST ? TP0 : TP0 + s2 - 1;
+    const int items = (LAST ? npos : cnt) * Lt * CW;
+    const T f = (T)P.scale;
+    for (int it = threadIdx.x; it < items; it += KC_THREADS) {
+        const int col = it % CW, q = it / CW, j = q % Lt, p = q / Lt;
+        const C a0 = src[(p * Lt + j) * CW + col], a1 = src[((p + s2) * Lt + j) * CW + col];
+        const C a2 = src[((p + 2 * s2) * Lt + j) * CW + col];
+        const C a3 = src[((p + 3 * s2) * Lt + j) * CW + col];
+        const C w1a = stw[j << (M0 - 1 - t)], w1b = stw[(j + Lt) << (M0 - 1 - t)];
+        const C b0 = bfly<EXACT>(a0, w1a, a2), b1 = bfly<EXACT>(a0, w1b, a2);  // level t+1 at p
+        const C c0v = bfly<EXACT>(a1, w1a, a3), c1 = bfly<EXACT>(a1, w1b, a3);  // at p + s_{t+2}
+        C o[4];
+        o[0] = bfly<EXACT>(b0, stw[j << (M0 - 2 - t)], c0v);
+        o[1] = bfly<EXACT>(b1, stw[(j + Lt) << (M0 - 2 - t)], c1);
+        o[2] = bfly<EXACT>(b0, stw[(j + 2 * Lt) << (M0 - 2 - t)], c0v);
+        o[3] = bfly<EXACT>(b1, stw[(j + 3 * Lt) << (M0 - 2 - t)], c1);
+        if constexpr (LAST) {
+            if (col >= ncol) continue;
+            const int64_t cc = c0 + col;
+            const int64_t p1 = cc >> P.m1, k1 = cc & ((1 << P.m1) - 1);
+            C *o_ = static_cast<C *>(P.out) +
+                    ((((r0 + p) * P.P1 + p1) * n0 + j) << P.m1) + k1;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                st_stream(o_ + ((int64_t)(u * Lt) << P.m1), P.apply_scale ? cscale(o[u], f) : o[u]);
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) dst[(p * 4 * Lt + j + u * Lt) * CW + col] = o[u];
+        }
+    }
+}
+
+template <typename T, bool EXACT, int M0, int TP0, int CW, bool LAST>
+__device__ __forceinline__ void kc_pass2(const cplx<T> *src, cplx<T> *dst, const cplx<T> *stw,
+                                         int npos, int ncol, const KCParams &P, int64_t r0,
+                                         int64_t c0) {
+    // levels 0 -> 1 (m0 odd), or the whole tree when m0 = 1
+    using C = cplx<T>;
+    constexpr int n0 = 1 << M0, s1 = n0 >> 1;
+    constexpr int cnt = LAST ? TP0 : TP0 + s1 - 1;
+    const int items = (LAST ? npos : cnt) * CW;
+    const C wa = stw[0], wb = stw[1 << (M0 - 1)];
+    const T f = (T)P.scale;
+    for (int it = threadIdx.x; it < items; it += KC_THREADS) {
+        const int col = it % CW, p = it / CW;
+        const C a0 = src[p * CW + col], a1 = src[(p + s1) * CW + col];
+        C lo = bfly<EXACT>(a0, wa, a1), hi = bfly<EXACT>(a0, wb, a1);
+        if constexpr (LAST) {
+            if (col >= ncol) continue;
+            const int64_t cc = c0 + col;
+            const int64_t p1 = cc >> P.m1, k1 = cc & ((1 << P.m1) - 1);
+            C *o_ = static_cast<C *>(P.out) + ((((r0 + p) * P.P1 + p1) * n0) << P.m1) + k1;
+            st_stream(o_, P.apply_scale ? cscale(lo, f) : lo);
+            st_stream(o_ + ((int64_t)1 << P.m1), P.apply_scale ? cscale(hi, f) : hi);
+        } else {
+            dst[(p * 2) * CW + col] = lo;
+            dst[(p * 2 + 1) * CW + col] = hi;
+        }
+    }
+}
+
+template <typename T, bool EXACT, int M0>
+__global__ void __launch_bounds__(KC_THREADS) kc_cols_kernel(const __grid_constant__ KCParams P) {
+    using C = cplx<T>;
+    using S = KCShape<T, M0>;
+    constexpr int n0 = 1 << M0, TP0 = S::TP0, CW = S::CW;
+    constexpr int W = TP0 + n0 - 1;
+    extern __shared__ __align__(16) unsigned char kc_smem_raw[];
+    C *bufA = reinterpret_cast<C *>(kc_smem_raw);
+    C *bufB = bufA + CW * kc_buf(M0, TP0, 0);
+    C *stw = bufB + CW * kc_buf(M0, TP0, 1);  // Omega_n0[k] (make_twiddles(1024), stride 1024/n0)
+    for (int k = threadIdx.x; k < n0; k += KC_THREADS)
+        stw[k] = __ldg(static_cast<const C *>(P.tw) + (k << (10 - M0)));
+    const C *z = static_cast<const C *>(P.z);
+    const int64_t ctiles = (P.cols + CW - 1) / CW;
+    const int64_t ntiles = ctiles * ((P.P0s + TP0 - 1) / TP0);
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t rt = tile / ctiles, ct = tile - rt * ctiles;
+        const int64_t r0 = rt * TP0, c0 = ct * CW;
+        const int npos = (int)(P.P0s - r0 < TP0 ? P.P0s - r0 : TP0);
+        const int ncol = (int)(P.cols - c0 < CW ? P.cols - c0 : CW);
+        __syncthreads();  // previous tile done with the buffers (and stw filled)
+        for (int it = threadIdx.x; it < W * CW; it += KC_THREADS) {  // level 0 = Z rows
+            const int col = it % CW, p = it / CW;
+            const int64_t r = r0 + p;
+            bufA[it] = (col < ncol && r < P.zrows) ? z[r * P.cols + c0 + col] : mk<T>((T)0, (T)0);
+        }
+        __syncthreads();
+        if constexpr (M0 == 1) {
+            kc_pass2<T, EXACT, M0, TP0, CW, true>(bufA, nullptr, stw, npos, ncol, P, r0, c0);
+        } else {
+            constexpr int T0 = M0 % 2;
+            C *src = bufA, *dst = bufB;
+            if constexpr (T0 == 1) {
+                kc_pass2<T, EXACT, M0, TP0, CW, false>(src, dst, stw, npos, ncol, P, r0, c0);
+                __syncthreads();
+                src = bufB;
+                dst = bufA;
+            }
+            static_for<(M0 - T0) / 2>([&](auto kcc) {
+                constexpr int t = T0 + 2 * decltype(kcc)::value;
+                if constexpr (t + 2 == M0) {
+                    kc_pass4<T, EXACT, M0, TP0, CW, t, true>(src, nullptr, stw, npos, ncol, P, r0, c0);
+                } else {
+                    kc_pass4<T, EXACT, M0, TP0, CW, t, false>(src, dst, stw, npos, ncol, P, r0, c0);
+                    __syncthreads();
+                    C *tmp = src;
+                    src = dst;
+                    dst = tmp;
+                }
+            });
+        }
+    }
+}
+
+template <typename T, bool EXACT, int M0>
+static int kc_launch_t(const KCParams &P, cudaStream_t st, int64_t *rows_per_strip_hint) {
+    using S = KCShape<T, M0>;
+    auto fn = &kc_cols_kernel<T, EXACT, M0>;
+    if (S::SMEM > 48 * 1024 &&
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM) !=
+            cudaSuccess)
+        return -2;
+    if (rows_per_strip_hint) *rows_per_strip_hint = S::TP0;
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, KC_THREADS, S::SMEM) != cudaSuccess ||
+        occ < 1)
+        return -2;
+    const int64_t tiles = ((P.cols + S::CW - 1) / S::CW) * ((P.P0s + S::TP0 - 1) / S::TP0);
+    if (tiles == 0) return 0;
+    const int64_t slots = (int64_t)P.sms * occ;
+    fn<<<(unsigned)(tiles < slots ? tiles : slots), KC_THREADS, S::SMEM, st>>>(P);
+    return 0;
+}
+
+template <typename T, bool EXACT>
+static int kc_dispatch(const KCParams &P, int m0, cudaStream_t st) {
+    switch (m0) {
+    case 1: return kc_launch_t<T, EXACT, 1>(P, st, nullptr);
+    case 2: return kc_launch_t<T, EXACT, 2>(P, st, nullptr);
+    case 3: return kc_launch_t<T, EXACT, 3>(P, st, nullptr);
+    case 4: return kc_launch_t<T, EXACT, 4>(P, st, nullptr);
+    case 5: return kc_launch_t<T, EXACT, 5>(P, st, nullptr);
+    case 6: return kc_launch_t<T, EXACT, 6>(P, st, nullptr);
+    case 7: return kc_launch_t<T, EXACT, 7>(P, st, nullptr);
+    case 8: return kc_launch_t<T, EXACT, 8>(P, st, nullptr);
+    case 9: return kc_launch_t<T, EXACT, 9>(P, st, nullptr);
+    case 10: return kc_launch_t<T, EXACT, 10>(P, st, nullptr);
+    default: return -3;
+    }
+}
+
+int launch_kc(const KCParams &P, int m0, int prec, cudaStream_t stream) {
+    return prec == 1 ? kc_dispatch<double, true>(P, m0, stream)
+                     : kc_dispatch<float, false>(P, m0, stream);
+}
+
+}  // namespace swdft2d

@@ -65,6 +65,22 @@ struct KRParams {
 // 0 ok, -2 shared-memory attribute / occupancy refused, -3 m1 out of range
 int launch_kr(const KRParams &P, int m1, int prec, cudaStream_t stream);
 
+// KC: column-tree kernel of the large-window path (kc_cols.cu), n0 = 2 .. 1024.
+struct KCParams {
+    const void *z;     // stage-R rows of the strip: [zrows][cols] complex of the precision
+    int64_t cols;      // P1 * n1
+    int64_t zrows;     // P0s + n0 - 1
+    int64_t P0s;       // window rows of the strip
+    int64_t P1;
+    int m1;
+    int apply_scale;
+    void *out;         // the strip's first output row: [P0s][P1][n0][n1]
+    double scale;
+    const void *tw;    // device make_twiddles(K0_TW_N) of the precision
+    int sms;
+};
+int launch_kc(const KCParams &P, int m0, int prec, cudaStream_t stream);
+
 // K2: one incremental stream push (k2_push.cu).
 struct K2Params {
     const void *row;  // the pushed row, N1 elements of in_dtype

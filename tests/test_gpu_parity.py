@@ -363,13 +363,15 @@ def test_sharded_api_world1(cuda):
 
 
 def test_large_windows_k0_and_unsupported(cuda, oracle_lib):
-    """Windows above K1's 2^6 run on K0 (bitwise); above 2^10 the ABI refuses loudly."""
+    """Windows above K1's 2^6 run on the large-window path and on K0 (both bitwise);
+    above 2^10 the ABI refuses loudly."""
     from paper_1707_08213_b200 import UnsupportedError
 
     rng = np.random.default_rng(12)
     x = rng.standard_normal((140, 12)) + 1j * rng.standard_normal((140, 12))
     ref = oracle_lib.tree2d(x, 7, 2)
-    assert bits_equal(run(x, 7, 2, "fp64"), ref)                   # auto -> K0 (m0 = 7)
+    assert bits_equal(run(x, 7, 2, "fp64"), ref)                   # auto -> KR + KC (m0 = 7)
+    assert bits_equal(run(x, 7, 2, "fp64", kernel="window"), ref)  # K0
     assert rel_err(run(x.astype(np.complex64), 7, 2, "fp32"), ref) <= FP32_TOL
     with pytest.raises(UnsupportedError):
         run(x, 7, 2, "fp64", kernel="stream")                     # K1 not instantiated
@@ -407,6 +409,35 @@ def test_row_kernel_windows(cuda, oracle_lib, m1):
     spec = WindowSpec((0, m1), "unitary")
     refu = oracle_lib.tree2d(x, 0, m1, scale=normalization_factor(spec))
     assert bits_equal(run(x, 0, m1, "fp64", normalization="unitary"), refu)
+
+
+@pytest.mark.parametrize("m", [(7, 2), (2, 7), (7, 7), (1, 8), (8, 1), (10, 3), (3, 10), (6, 9),
+                               (3, 3), (4, 4), (1, 1), (5, 0)])
+def test_separable_large_windows(cuda, oracle_lib, m):
+    """KR + KC (the large-window path, also forced on small windows): bitwise vs the
+    oracle in fp64 with unitary scale, strided rows, window-row ranges; fp32 in tolerance."""
+    from paper_1707_08213_b200.core import normalization_factor
+
+    m0, m1 = m
+    n0, n1 = 1 << m0, 1 << m1
+    rng = np.random.default_rng(7 * m0 + m1)
+    N0, N1 = n0 + 5 + (m0 * 7) % 11, n1 + 9 + (m1 * 5) % 13
+    x = rng.standard_normal((N0, N1)) + 1j * rng.standard_normal((N0, N1))
+    spec = WindowSpec(m, "unitary")
+    ref = oracle_lib.tree2d(x, m0, m1, scale=normalization_factor(spec))
+    kern = "auto" if max(m) > 6 else "separable"
+    got = run(x, m0, m1, "fp64", kernel=kern, normalization="unitary")
+    assert bits_equal(got, ref)
+    assert rel_err(run(x.astype(np.complex64), m0, m1, "fp32", kernel=kern,
+                       normalization="unitary"), ref) <= FP32_TOL
+    wide = torch.zeros((N0, N1 + 3), dtype=torch.complex128, device=cuda)
+    wide[:, :N1] = torch.from_numpy(x).to(cuda)
+    P0, P1 = N0 - n0 + 1, N1 - n1 + 1
+    a, b = min(2, P0 - 1), P0
+    part = torch.empty((b - a, P1, n0, n1), dtype=torch.complex128, device=cuda)
+    forward_into(wide[:, :N1], m0, m1, part, prec=_lib.PREC_FP64, p0_begin=a, p0_end=b,
+                 kernel="separable", scale=normalization_factor(spec))
+    assert bits_equal(part.cpu().numpy(), ref[a:b])
 
 
 def test_row_kernel_1d_large_and_errors(cuda, oracle_lib):
