@@ -169,6 +169,18 @@ int swdft2d_stream_push(const void *row, int in_dtype, int64_t N1, void *ring, v
 /* Bytes of the incremental stream state: (m0 * n0/2 + n0 - 1) * P1 * n1 complex of prec. */
 int swdft2d_stream_state_bytes(int64_t N1, int m0, int m1, int prec, int64_t *bytes);
 
+/*
+ * The dim-0 tree down every column of a complex matrix z ([N0][cols], row stride ld_z,
+ * complex of prec), written in the layout of the reference's k-D output:
+ * out[p0 - p0_begin][c >> m_inner][k0][c & (2^m_inner - 1)].  The last level block of
+ * treekd.tree_swdft_kd (treekd.py:102-121, kd_level_step for dimension 0) over the
+ * stacked results of the inner dimensions, with the transpose of k0 into place fused
+ * (KC).  1 <= m0 <= 10; cols a multiple of 2^m_inner.
+ */
+int swdft2d_forward_columns(const void *z, int prec, int64_t N0, int64_t cols, int64_t ld_z, int m0,
+                            int m_inner, double scale, int64_t p0_begin, int64_t p0_end, void *out,
+                            void *stream);
+
 /* Frees cached per-device state (twiddle tables).  Safe to call twice. */
 int swdft2d_shutdown(void);
 

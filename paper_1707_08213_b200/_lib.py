@@ -53,6 +53,8 @@ SIGNATURES = {
     "swdft2d_stream_push": (_int, [_vp, _int, _i64, _vp, _vp, _int, _int, _int, _dbl, _i64, _vp,
                                    _int, _vp]),
     "swdft2d_stream_state_bytes": (_int, [_i64, _int, _int, _int, _pi64]),
+    "swdft2d_forward_columns": (_int, [_vp, _int, _i64, _i64, _i64, _int, _int, _dbl, _i64, _i64,
+                                       _vp, _vp]),
     "swdft2d_shutdown": (_int, []),
 }
 

@@ -289,6 +289,7 @@ static int forward_separable(const void *x, int in_dtype, int64_t N1, int64_t ld
         std::memset(&c, 0, sizeof c);
         c.z = z;
         c.cols = cols;
+        c.ldz = cols;
         c.zrows = b - a + n0 - 1;
         c.P0s = b - a;
         c.P1 = P1;
@@ -682,6 +683,55 @@ int swdft2d_stream_push(const void *row, int in_dtype, int64_t N1, void *ring, v
     const void *win = static_cast<const char *>(ring) + first * N1 * eb;
     return swdft2d_forward(win, prec == SWDFT2D_PREC_FP64 ? SWDFT2D_IN_C128 : SWDFT2D_IN_C64, n0,
                            N1, N1, m0, m1, prec, scale, 0, 1, out, kernel, stream);
+}
+
+int swdft2d_forward_columns(const void *z, int prec, int64_t N0, int64_t cols, int64_t ld_z, int m0,
+                            int m_inner, double scale, int64_t p0_begin, int64_t p0_end, void *out,
+                            void *stream) {
+    if (prec != SWDFT2D_PREC_FP32 && prec != SWDFT2D_PREC_FP64)
+        return fail(SWDFT2D_E_INVALID_ARG, "unknown precision code %d", prec);
+    if (m0 < 1 || m0 > SWDFT2D_K0_MAX_M)
+        return fail(SWDFT2D_E_UNSUPPORTED, "column trees need 1 <= m0 <= %d (got %d)",
+                    SWDFT2D_K0_MAX_M, m0);
+    if (m_inner < 0 || m_inner > 40 || cols < 1 || (cols & (((int64_t)1 << m_inner) - 1)) != 0)
+        return fail(SWDFT2D_E_INVALID_ARG, "cols %lld is not a multiple of 2^%d", (long long)cols,
+                    m_inner);
+    if (ld_z < cols) return fail(SWDFT2D_E_INVALID_ARG, "ld_z %lld < cols %lld", (long long)ld_z, (long long)cols);
+    const int64_t n0 = (int64_t)1 << m0;
+    if (n0 > N0)
+        return fail(SWDFT2D_E_WINDOW_TOO_LARGE, "window size %lld exceeds extent %lld in dimension 0",
+                    (long long)n0, (long long)N0);
+    const int64_t P0 = N0 - n0 + 1;
+    if (p0_begin < 0 || p0_end > P0 || p0_begin > p0_end)
+        return fail(SWDFT2D_E_INVALID_ARG, "window rows [%lld, %lld) outside [0, %lld)",
+                    (long long)p0_begin, (long long)p0_end, (long long)P0);
+    if (p0_begin == p0_end) return SWDFT2D_OK;
+    if (!z || !out) return fail(SWDFT2D_E_INVALID_ARG, "null device pointer");
+    DeviceState *ds = nullptr;
+    int rc = device_state(&ds);
+    if (rc) return rc;
+    const void *tw64 = nullptr, *tw32 = nullptr;
+    if ((rc = k0_tables(ds, &tw64, &tw32))) return rc;
+    const int64_t esz = prec == SWDFT2D_PREC_FP64 ? 16 : 8;
+    KCParams c;
+    std::memset(&c, 0, sizeof c);
+    c.z = static_cast<const char *>(z) + p0_begin * ld_z * esz;
+    c.cols = cols;
+    c.ldz = ld_z;
+    c.zrows = p0_end - p0_begin + n0 - 1;
+    c.P0s = p0_end - p0_begin;
+    c.P1 = cols >> m_inner;
+    c.m1 = m_inner;
+    c.apply_scale = scale == 1.0 ? 0 : 1;
+    c.scale = scale;
+    c.out = out;
+    c.tw = prec == SWDFT2D_PREC_FP64 ? tw64 : tw32;
+    c.sms = ds->sms;
+    if (launch_kc(c, m0, prec, reinterpret_cast<cudaStream_t>(stream)))
+        return fail(SWDFT2D_E_CUDA, "column-tree launch setup failed (m0=%d)", m0);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(SWDFT2D_E_CUDA, "column-tree launch: %s", cudaGetErrorString(e));
+    return SWDFT2D_OK;
 }
 
 int swdft2d_shutdown(void) {

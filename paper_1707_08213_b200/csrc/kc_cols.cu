@@ -78,7 +78,7 @@ __device__ __forceinline__ void kc_pass4(const cplx<T> *src, cplx<T> *dst, const
         if constexpr (LAST) {
             if (col >= ncol) continue;
             const int64_t cc = c0 + col;
-            const int64_t p1 = cc >> P.m1, k1 = cc & ((1 << P.m1) - 1);
+            const int64_t p1 = cc >> P.m1, k1 = cc & (((int64_t)1 << P.m1) - 1);
             C *o_ = static_cast<C *>(P.out) +
                     ((((r0 + p) * P.P1 + p1) * n0 + j) << P.m1) + k1;
 #pragma unroll
@@ -109,7 +109,7 @@ __device__ __forceinline__ void kc_pass2(const cplx<T> *src, cplx<T> *dst, const
         if constexpr (LAST) {
             if (col >= ncol) continue;
             const int64_t cc = c0 + col;
-            const int64_t p1 = cc >> P.m1, k1 = cc & ((1 << P.m1) - 1);
+            const int64_t p1 = cc >> P.m1, k1 = cc & (((int64_t)1 << P.m1) - 1);
             C *o_ = static_cast<C *>(P.out) + ((((r0 + p) * P.P1 + p1) * n0) << P.m1) + k1;
             st_stream(o_, P.apply_scale ? cscale(lo, f) : lo);
             st_stream(o_ + ((int64_t)1 << P.m1), P.apply_scale ? cscale(hi, f) : hi);
@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(KC_THREADS) kc_cols_kernel(const __grid_consta
         for (int it = threadIdx.x; it < W * CW; it += KC_THREADS) {  // level 0 = Z rows
             const int col = it % CW, p = it / CW;
             const int64_t r = r0 + p;
-            bufA[it] = (col < ncol && r < P.zrows) ? z[r * P.cols + c0 + col] : mk<T>((T)0, (T)0);
+            bufA[it] = (col < ncol && r < P.zrows) ? z[r * P.ldz + c0 + col] : mk<T>((T)0, (T)0);
         }
         __syncthreads();
         if constexpr (M0 == 1) {

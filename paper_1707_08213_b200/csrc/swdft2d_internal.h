@@ -68,11 +68,12 @@ int launch_kr(const KRParams &P, int m1, int prec, cudaStream_t stream);
 // KC: column-tree kernel of the large-window path (kc_cols.cu), n0 = 2 .. 1024.
 struct KCParams {
     const void *z;     // stage-R rows of the strip: [zrows][cols] complex of the precision
-    int64_t cols;      // P1 * n1
+    int64_t cols;      // P1 * n1 (columns transformed)
+    int64_t ldz;       // row stride of z, elements (>= cols)
     int64_t zrows;     // P0s + n0 - 1
     int64_t P0s;       // window rows of the strip
-    int64_t P1;
-    int m1;
+    int64_t P1;        // cols >> m1
+    int m1;            // output layout [P0s][P1][n0][2^m1]: column c = (c >> m1, c & (2^m1 - 1))
     int apply_scale;
     void *out;         // the strip's first output row: [P0s][P1][n0][n1]
     double scale;

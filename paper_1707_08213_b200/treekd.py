@@ -6,11 +6,12 @@ first block of levels and dimension 0 the last (core.py:150-161), and every leve
 combines positions along its own dimension only.  So for k >= 3:
 
   1. levels of dims k-1 .. 1 act on each slice x[i0] independently: they are the
-     (k-1)-dimensional tree of that slice (computed recursively; k-1 = 2 is K1);
+     (k-1)-dimensional tree of that slice (computed recursively; for k = 3 all
+     slices go through one K1 launch over the slices stacked as a 2-D array);
   2. levels of dim 0 are, for every (p_1.., k_1..) column of the stacked slice
-     results, the 1D tree along i0 with window n0 — K1 with m1 = 0 on the
-     [N0, prod(inner)] matrix of slice results;
-  3. a transpose moves k0 from the last axis to axis k.
+     results, the 1D tree along i0 with window n0 — the column-tree kernel KC
+     (swdft2d_forward_columns) on the [N0, prod(inner)] matrix of slice results,
+     which writes k0 straight into axis k (no separate transpose pass).
 
 Each node is computed by the same butterfly with the same operands as in the
 reference's lattice, so fp64 output is bit-identical (tests/test_next_rows.py).
@@ -22,7 +23,7 @@ import math
 
 import torch
 
-from . import core
+from . import _lib, core
 from .core import CoefficientArray
 from .tree2d import _OUT_DTYPES, _precision_code, _to_tensor, forward_into
 
@@ -43,38 +44,55 @@ def level_regions_kd(shape, exponents):
     return out
 
 
-def _kd_values(xt: torch.Tensor, exps, prec: int, scale: float) -> torch.Tensor:
-    """Unnormalized-then-scaled coefficients of a k-D device array (k >= 1)."""
+def _kd_values(xt: torch.Tensor, exps, prec: int, scale: float, out=None) -> torch.Tensor:
+    """Unnormalized-then-scaled coefficients of a k-D device array (k >= 1), written into
+    ``out`` (shape (P_0.., n_0..)) when given."""
     k = len(exps)
     dev = xt.device
     odt = _OUT_DTYPES[prec]
+    sizes = [1 << m for m in exps]
+    P = [int(N) - n + 1 for N, n in zip(xt.shape, sizes)]
+    if out is None:
+        out = torch.empty(tuple(P) + tuple(sizes), dtype=odt, device=dev)
     if k == 1:
         (m,) = exps
-        N = xt.shape[0]
-        out = torch.empty((1, N - (1 << m) + 1, 1, 1 << m), dtype=odt, device=dev)
-        forward_into(xt.reshape(1, N), 0, m, out, prec=prec, scale=scale)
-        return out.view(N - (1 << m) + 1, 1 << m)
-    if k == 2:
-        m0, m1 = exps
-        out = torch.empty((xt.shape[0] - (1 << m0) + 1, xt.shape[1] - (1 << m1) + 1, 1 << m0,
-                           1 << m1), dtype=odt, device=dev)
-        forward_into(xt if xt.stride(-1) == 1 else xt.contiguous(), m0, m1, out, prec=prec,
+        forward_into(xt.reshape(1, -1), 0, m, out.view(1, P[0], 1, sizes[0]), prec=prec,
                      scale=scale)
         return out
-    m0 = exps[0]
-    n0 = 1 << m0
-    N0 = xt.shape[0]
-    P0 = N0 - n0 + 1
-    inner = torch.stack([_kd_values(xt[i], exps[1:], prec, 1.0) for i in range(N0)])
-    inner_shape = inner.shape[1:]  # (P1 .. P_{k-1}, n1 .. n_{k-1})
-    M = math.prod(inner_shape)
-    col = torch.empty((P0, M, n0, 1), dtype=odt, device=dev)
-    forward_into(inner.reshape(N0, M), m0, 0, col, prec=prec, scale=scale)
-    kk = k - 1
-    # [P0, P1.., n1.., n0] -> [P0, P1.., n0, n1..]
-    v = col.view((P0,) + tuple(inner_shape) + (n0,))
-    perm = [0] + [1 + i for i in range(kk)] + [1 + 2 * kk] + [1 + kk + i for i in range(kk)]
-    return v.permute(perm).contiguous()
+    if k == 2:
+        forward_into(xt if xt.stride(-1) == 1 else xt.contiguous(), exps[0], exps[1], out,
+                     prec=prec, scale=scale)
+        return out
+    # dims k-1 .. 1: the (k-1)-D tree of every slice x[i0], straight into the stacked
+    # matrix of slice results; then dim 0 down its columns with k0 put in place (KC)
+    m0, n0, N0, P0 = exps[0], sizes[0], int(xt.shape[0]), P[0]
+    M = math.prod(P[1:]) * math.prod(sizes[1:])
+    if k == 3:
+        # every slice's 2-D transform in ONE K1 launch: the slices stacked as an
+        # (N0 N1) x N2 array; window rows that straddle two slices are computed into
+        # the gap rows (p1 >= P1 of each slice) and never read
+        N1, N2 = int(xt.shape[1]), int(xt.shape[2])
+        x2 = xt.contiguous().view(N0 * N1, N2)
+        ld = N1 * P[2] * sizes[1] * sizes[2]
+        stacked = torch.empty((N0 * N1, P[2], sizes[1], sizes[2]), dtype=odt, device=dev)
+        forward_into(x2, exps[1], exps[2], stacked[:N0 * N1 - sizes[1] + 1], prec=prec)
+        inner = stacked.view(N0, ld)[:, :M]
+    else:
+        inner = torch.empty((N0,) + tuple(P[1:]) + tuple(sizes[1:]), dtype=odt, device=dev)
+        for i in range(N0):
+            _kd_values(xt[i], exps[1:], prec, 1.0, out=inner[i])
+        inner = inner.view(N0, M)
+        ld = M
+    if m0 == 0:
+        v = inner.reshape(out.shape)
+        return out.copy_(v * scale if scale != 1.0 else v)
+    lib = _lib.load()
+    with torch.cuda.device(dev):
+        rc = lib.swdft2d_forward_columns(inner.data_ptr(), prec, N0, M, ld, m0, sum(exps[1:]),
+                                         float(scale), 0, P0, out.data_ptr(),
+                                         torch.cuda.current_stream(dev).cuda_stream)
+    _lib.check(rc)
+    return out
 
 
 def tree_swdft_kd(x, spec, counter=None, budget=None, *, precision=None,

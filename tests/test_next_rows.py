@@ -348,3 +348,26 @@ def test_stream1d_equals_batch(cuda, m):
     assert all(g is None for g in got[:n - 1])
     g = np.stack([x.cpu().numpy() for x in got[n - 1:]])
     assert np.array_equal(g.view(np.uint64), ref.view(np.uint64))
+
+
+@pytest.mark.gpu
+def test_treekd_columns_and_m0_zero(cuda):
+    """3-D and 4-D through the column-tree pass: equal (fp64 bits) to composing the
+    2-D drop-in per slice and a dim-0 tree computed with the 1-D drop-in along i0;
+    a window with n0 = 1 equals the per-slice 2-D result."""
+    from paper_1707_08213_b200 import tree_swdft_2d
+    from paper_1707_08213_b200.tree1d import tree_swdft_1d
+    from paper_1707_08213_b200.treekd import tree_swdft_kd
+
+    rng = np.random.default_rng(91)
+    x = rng.standard_normal((19, 12, 14)) + 1j * rng.standard_normal((19, 12, 14))
+    v = tree_swdft_kd(x, WindowSpec((3, 2, 3))).values.cpu().numpy()   # (P0,P1,P2,n0,n1,n2)
+    sl = np.stack([tree_swdft_2d(x[i], WindowSpec((2, 3))).values.cpu().numpy()
+                   for i in range(19)])                               # (N0,P1,P2,n1,n2)
+    col = sl.reshape(19, -1)
+    ref = np.stack([tree_swdft_1d(col[:, j], WindowSpec((3,))).values.cpu().numpy()
+                    for j in range(col.shape[1])], axis=1)            # (P0, M, n0)
+    ref = np.ascontiguousarray(ref.reshape((12, 9, 7, 4, 8, 8)).transpose(0, 1, 2, 5, 3, 4))
+    assert np.array_equal(v.view(np.uint64), ref.view(np.uint64))
+    v0 = tree_swdft_kd(x, WindowSpec((0, 2, 3))).values.cpu().numpy()
+    assert np.array_equal(v0.view(np.uint64), sl.reshape(19, 9, 7, 1, 4, 8).view(np.uint64))
