@@ -8,14 +8,15 @@ mirrors /root/reference/pkg/src/swdft/tree2d.py:175-202: same arguments, the
 same validation order and exceptions, the same [P0, P1, n0, n1] layout, twiddle
 sign and index convention, the same budget accounting, the same OpCounter
 calls, and the same normalization bookkeeping.  The compute runs in
-libswdft2d.so (K1 fused streaming kernel) on the current torch stream;
+libswdft2d.so on the current torch stream (K1, the fused streaming kernel, for
+windows up to 64x64; KR for n0 = 1; KR + KC for larger windows up to 1024x1024);
 ``values`` of the returned CoefficientArray is a device-resident torch tensor
 (complex128 for precision "fp64" — bitwise equal to the reference — or
 complex64 for "fp32").  PyTorch only provides device buffers and the stream.
 
 Differences a caller can observe, all deliberate:
   * ``loop_order`` is validated, then has no effect: the reference's two
-    schedules are bitwise identical (tree2d.py:185-186), and so is K1's.
+    schedules are bitwise identical (tree2d.py:185-186), and so are the kernels'.
   * ``threads`` is accepted and ignored (there are no host threads).
   * ``precision`` defaults to "fp32" for float32/complex64 input and "fp64"
     otherwise; the reference always computes in complex128.
