@@ -15,7 +15,7 @@
 namespace swdft2d {
 
 constexpr int KC_THREADS = 256;
-constexpr size_t KC_SMEM_CAP = 100 * 1024;
+constexpr size_t KC_SMEM_CAP = 113 * 1024;  // two CTAs per SM
 
 // nodes of level t for TP0 window rows: (TP0 + s_t - 1) 2^t, per column
 __host__ __device__ constexpr int64_t kc_level_nodes(int M0, int TP0, int t) {
@@ -41,13 +41,13 @@ __host__ __device__ constexpr size_t kc_smem(int M0, int TP0, int CW, int esz) {
 // tile shape: the widest column group (then the most window rows) within the cap
 template <typename T, int M0> struct KCShape {
     static constexpr int pick(int what) {
-        const int cws[5] = {32, 16, 8, 4, 2};
-        const int tps[3] = {16, 8, 4};
-        for (int a = 0; a < 5; ++a)
-            for (int b = 0; b < 3; ++b)
+        const int cws[6] = {32, 16, 8, 4, 2, 1};
+        const int tps[4] = {16, 8, 4, 2};
+        for (int a = 0; a < 6; ++a)
+            for (int b = 0; b < 4; ++b)
                 if (kc_smem(M0, tps[b], cws[a], (int)sizeof(T) * 2) <= KC_SMEM_CAP)
                     return what == 0 ? cws[a] : tps[b];
-        return what == 0 ? 1 : 1;
+        return 1;
     }
     static constexpr int CW = pick(0), TP0 = pick(1);
     static constexpr size_t SMEM = kc_smem(M0, TP0, CW, (int)sizeof(T) * 2);
@@ -135,16 +135,47 @@ __global__ void __launch_bounds__(KC_THREADS) kc_cols_kernel(const __grid_consta
     const C *z = static_cast<const C *>(P.z);
     const int64_t ctiles = (P.cols + CW - 1) / CW;
     const int64_t ntiles = ctiles * ((P.P0s + TP0 - 1) / TP0);
+    // level 0 (the tile's W Z rows x CW columns) of the NEXT tile is loaded into
+    // registers while the current tile's passes run
+    constexpr int NLOAD = (W * CW + KC_THREADS - 1) / KC_THREADS;
+    // prefetch unless the column group is narrow (scattered 16-32 B row pieces: measured
+    // slower for n0 = 1024) or the tile too large for registers
+    constexpr bool PF = NLOAD <= 20 && CW >= 8;
+    constexpr int NPRE = PF ? NLOAD : 1;
+    C pre[NPRE];
+    auto fetch = [&](int64_t tile) {
+        const int64_t rt = tile / ctiles, ct = tile - rt * ctiles;
+        const int64_t r0 = rt * TP0, c0 = ct * CW;
+        const int ncol = (int)(P.cols - c0 < CW ? P.cols - c0 : CW);
+#pragma unroll
+        for (int q = 0; q < NPRE; ++q) {
+            const int it = threadIdx.x + q * KC_THREADS;
+            const int col = it % CW, p = it / CW;
+            const int64_t r = r0 + p;
+            pre[q] = (it < W * CW && col < ncol && r < P.zrows) ? z[r * P.ldz + c0 + col]
+                                                                : mk<T>((T)0, (T)0);
+        }
+    };
+    if (PF && (int64_t)blockIdx.x < ntiles) fetch(blockIdx.x);
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t rt = tile / ctiles, ct = tile - rt * ctiles;
         const int64_t r0 = rt * TP0, c0 = ct * CW;
         const int npos = (int)(P.P0s - r0 < TP0 ? P.P0s - r0 : TP0);
         const int ncol = (int)(P.cols - c0 < CW ? P.cols - c0 : CW);
         __syncthreads();  // previous tile done with the buffers (and stw filled)
-        for (int it = threadIdx.x; it < W * CW; it += KC_THREADS) {  // level 0 = Z rows
-            const int col = it % CW, p = it / CW;
-            const int64_t r = r0 + p;
-            bufA[it] = (col < ncol && r < P.zrows) ? z[r * P.ldz + c0 + col] : mk<T>((T)0, (T)0);
+        if constexpr (PF) {
+#pragma unroll
+            for (int q = 0; q < NPRE; ++q) {  // level 0 = Z rows
+                const int it = threadIdx.x + q * KC_THREADS;
+                if (it < W * CW) bufA[it] = pre[q];
+            }
+            if (tile + gridDim.x < ntiles) fetch(tile + gridDim.x);
+        } else {
+            for (int it = threadIdx.x; it < W * CW; it += KC_THREADS) {
+                const int col = it % CW, p = it / CW;
+                const int64_t r = r0 + p;
+                bufA[it] = (col < ncol && r < P.zrows) ? z[r * P.ldz + c0 + col] : mk<T>((T)0, (T)0);
+            }
         }
         __syncthreads();
         if constexpr (M0 == 1) {
