@@ -152,11 +152,17 @@ def cpu_reference_rate(cfg, rows: int, reps: int, threads: int):
     import oracle
 
     oracle.build()
+    try:  # the reference keeps the whole lattice in memory; bound it by the host's RAM
+        import psutil
+
+        cap = min(1 << 36, psutil.virtual_memory().available // 3)
+    except ImportError:
+        cap = 1 << 33
     x = cfg.generate(rows=rows + cfg.n0 - 1)
     times = []
     for _ in range(reps):
         t0 = time.perf_counter()
-        out = oracle.tree2d(x, cfg.m0, cfg.m1, threads=threads, max_lattice_bytes=1 << 36)
+        out = oracle.tree2d(x, cfg.m0, cfg.m1, threads=threads, max_lattice_bytes=cap)
         times.append(time.perf_counter() - t0)
     coefs = out.size
     del out
@@ -529,7 +535,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--ref-rows", type=int, default=128)
+    ap.add_argument("--ref-rows", type=int, default=None,
+                    help="window rows of the CPU sample (default: 64 for c5 as BASELINE.json "
+                         "says, else 128; c1/c2 are small enough to run whole)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -546,6 +554,8 @@ def main():
     from paper_1707_08213_b200.workloads import CONFIGS
 
     cfg = CONFIGS[args.config]
+    if args.ref_rows is None:
+        args.ref_rows = cfg.P0 if cfg.name in ("c1", "c2") else 64 if cfg.name == "c5" else 128
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
     local_rank = env_int("LOCAL_RANK", 0)
