@@ -177,7 +177,7 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
                     const int64_t col = pcol + lam + G * a;
                     xs[tt][a] = ((S::TASKS % S::WARPS) == 0 || task < S::TASKS) && row < in_end &&
                                         col < P.N1
-                                    ? load_x<T>(P.x, P.in_dtype, row * P.ldx + col)
+                                    ? load_raw<T>(P.x, P.in_dtype, row * P.ldx + col)
                                     : mk<T>(0, 0);
                 }
             }
@@ -215,7 +215,7 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
                                                   P.in_dtype);
                     } else {
 #pragma unroll
-                        for (int a = 0; a < V; ++a) s[a] = xs[tt][a];
+                        for (int a = 0; a < V; ++a) s[a] = from_raw<T>(xs[tt][a], P.in_dtype);
                     }
                     // in-register levels (n1 > 32): classes c = lam + G*a
 #pragma unroll

@@ -114,6 +114,55 @@ __device__ __forceinline__ cplx<T> load_x(const void *__restrict__ x, int in_dty
     }
 }
 
+// Prefetch form of load_x: the loaded bits are kept as they are (packed into the
+// complex<T> register pair when they fit) and converted by from_raw at use time, so a
+// prefetch never waits for its load (a conversion right after the load would).
+template <typename T>
+__device__ __forceinline__ cplx<T> load_raw(const void *__restrict__ x, int in_dtype, int64_t off);
+template <>
+__device__ __forceinline__ double2 load_raw<double>(const void *__restrict__ x, int in_dtype,
+                                                    int64_t off) {
+    switch (in_dtype) {
+    case 0: return make_double2(__hiloint2double(0, __float_as_int(__ldg((const float *)x + off))), 0.0);
+    case 1: return make_double2(__ldg((const double *)x + off), 0.0);
+    case 2: {
+        const float2 v = __ldg((const float2 *)x + off);
+        return make_double2(__hiloint2double(__float_as_int(v.y), __float_as_int(v.x)), 0.0);
+    }
+    default: return __ldg((const double2 *)x + off);
+    }
+}
+template <>
+__device__ __forceinline__ float2 load_raw<float>(const void *__restrict__ x, int in_dtype,
+                                                  int64_t off) {
+    switch (in_dtype) {
+    case 0: return make_float2(__ldg((const float *)x + off), 0.f);
+    case 1: {
+        const double d = __ldg((const double *)x + off);
+        return make_float2(__int_as_float(__double2loint(d)), __int_as_float(__double2hiint(d)));
+    }
+    case 2: return __ldg((const float2 *)x + off);
+    default: {  // 128-bit sample does not fit the float2 pair: convert now
+        const double2 v = __ldg((const double2 *)x + off);
+        return make_float2((float)v.x, (float)v.y);
+    }
+    }
+}
+template <typename T> __device__ __forceinline__ cplx<T> from_raw(cplx<T> r, int in_dtype);
+template <> __device__ __forceinline__ double2 from_raw<double>(double2 r, int in_dtype) {
+    switch (in_dtype) {
+    case 0: return make_double2((double)__int_as_float(__double2loint(r.x)), 0.0);
+    case 2: return make_double2((double)__int_as_float(__double2loint(r.x)),
+                                (double)__int_as_float(__double2hiint(r.x)));
+    default: return r;  // f64 (imaginary part already +0.0) and c128
+    }
+}
+template <> __device__ __forceinline__ float2 from_raw<float>(float2 r, int in_dtype) {
+    if (in_dtype == 1)
+        return make_float2((float)__hiloint2double(__float_as_int(r.y), __float_as_int(r.x)), 0.f);
+    return r;  // f32 (imaginary +0.0), c64, and c128 (converted at load)
+}
+
 // Sample of x staged in shared memory (TMA tile), element type in_dtype.
 template <typename T>
 __device__ __forceinline__ cplx<T> load_staged(const unsigned char *p, int in_dtype) {
