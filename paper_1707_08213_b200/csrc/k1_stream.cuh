@@ -374,9 +374,10 @@ constexpr K1Choice K1_TUNED_FP32[] = {
     {2, 3, 0, 32}, {3, 2, 0, 64}, {3, 4, 1, 2}, {4, 3, 2, 8}, {4, 6, 1, 1}, {5, 2, 3, 8},
     {5, 4, 3, 2},  {5, 6, 2, 1},  {6, 2, 3, 2}, {6, 3, 3, 2}, {6, 4, 3, 1}, {6, 5, 3, 1},
 };
-// fp64 (4,4): MINB 4 caps registers at 128 (157 uncapped, 3 CTAs/SM, latency-bound):
-// +13 % on config 2, +4 % on config 4 in bitwise mode (profiles/TUNING_r01.md)
-constexpr K1Choice K1_TUNED_FP64[] = {{3, 4, 1, 2}, {4, 4, 2, 2, 4}};
+// (A register cap, MINB 4, helped fp64 (4,4) while the input prefetch stalled on its
+// conversion; with raw-bit prefetch the uncapped kernel is faster on config 4:
+// 383 vs 368 Gcoef/s, profiles/TUNING_r01.md.)
+constexpr K1Choice K1_TUNED_FP64[] = {{3, 4, 1, 2}};
 constexpr int k1_choose_q(int M0, int M1, bool DBL = false) {
     for (const K1Choice &c : K1_TUNED_FP32)
         if (!DBL && c.m0 == M0 && c.m1 == M1) return c.q;

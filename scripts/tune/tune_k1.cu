@@ -5,6 +5,8 @@
 #include "../../paper_1707_08213_b200/csrc/k1_stream.cuh"
 #include "../../paper_1707_08213_b200/csrc/k0_window.cu"
 #include "../../paper_1707_08213_b200/csrc/k2_push.cu"
+#include "../../paper_1707_08213_b200/csrc/kr_rows.cu"
+#include "../../paper_1707_08213_b200/csrc/kc_cols.cu"
 
 namespace swdft2d {
 void k1_register_m0_0() {}
