@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(KR_THREADS) kr_rows_kernel(const __grid_consta
 #pragma unroll
         for (int r = 0; r < NPRE; ++r) {
             const int p = threadIdx.x + r * KR_THREADS;
-            pre[r] = (p < W && q0 + p < P.N1) ? load_x<T>(P.x, P.in_dtype, xrow + q0 + p)
+            pre[r] = (p < W && q0 + p < P.N1) ? load_raw<T>(P.x, P.in_dtype, xrow + q0 + p)
                                               : mk<T>((T)0, (T)0);
         }
     };
@@ -161,7 +161,7 @@ __global__ void __launch_bounds__(KR_THREADS) kr_rows_kernel(const __grid_consta
 #pragma unroll
         for (int r = 0; r < NPRE; ++r) {  // level 0: samples x[row, q0 .. q0 + W)
             const int p = threadIdx.x + r * KR_THREADS;
-            if (p < W) bufA[p] = pre[r];
+            if (p < W) bufA[p] = from_raw<T>(pre[r], P.in_dtype);
         }
         if (tile + gridDim.x < ntiles) fetch(tile + gridDim.x);
         __syncthreads();
