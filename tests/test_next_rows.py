@@ -371,3 +371,22 @@ def test_treekd_columns_and_m0_zero(cuda):
     assert np.array_equal(v.view(np.uint64), ref.view(np.uint64))
     v0 = tree_swdft_kd(x, WindowSpec((0, 2, 3))).values.cpu().numpy()
     assert np.array_equal(v0.view(np.uint64), sl.reshape(19, 9, 7, 1, 4, 8).view(np.uint64))
+
+
+@pytest.mark.gpu
+def test_row_stream_large_window(cuda, oracle_lib):
+    """Windows beyond K2's 64 (here 128 x 4): pushes re-run the large-window path over
+    the raw ring; slabs bitwise equal to the batch rows, blocks and singles mixed."""
+    from paper_1707_08213_b200.stream import SlidingRowStream2D
+
+    rng = np.random.default_rng(123)
+    x = rng.standard_normal((140, 20)) + 1j * rng.standard_normal((140, 20))
+    ref = oracle_lib.tree2d(x, 7, 2)
+    st = SlidingRowStream2D(WindowSpec((7, 2)), 20)
+    assert st._state is None
+    out = st.push_rows(x[:130])
+    got = [out.cpu().numpy()]
+    for r in range(130, 140):
+        got.append(st.push_row(x[r]).cpu().numpy()[None])
+    g = np.concatenate(got)
+    assert np.array_equal(g.view(np.uint64), ref.view(np.uint64))
