@@ -471,3 +471,18 @@ def test_host_output_pipeline(cuda, oracle_lib):
                           strip_bytes=1 << 12)
     assert res32.values.base is not None or res32.values.ctypes.data == host.data_ptr()
     assert rel_err(res32.values, ref) <= FP32_TOL
+
+
+@pytest.mark.parametrize("m0", list(range(0, 7)))
+def test_every_k1_window_fp64_bitwise_fp32_tol(cuda, oracle_lib, m0):
+    """Every window n0 x n1 with n0, n1 in 1..64 (all 49 K1 instantiations per
+    precision): fp64 bitwise vs the oracle, fp32 within tolerance, ragged extents."""
+    rng = np.random.default_rng(500 + m0)
+    for m1 in range(0, 7):
+        n0, n1 = 1 << m0, 1 << m1
+        N0, N1 = n0 + 3 + (m1 * 5) % 7, n1 + 2 + (m0 * 3) % 5
+        x = rng.standard_normal((N0, N1)) + 1j * rng.standard_normal((N0, N1))
+        ref = oracle_lib.tree2d(x, m0, m1)
+        kern = "stream" if m0 > 0 else "rows"
+        assert bits_equal(run(x, m0, m1, "fp64", kernel=kern), ref), (m0, m1)
+        assert rel_err(run(x.astype(np.complex64), m0, m1, "fp32", kernel=kern), ref) <= FP32_TOL
