@@ -133,3 +133,14 @@ def stream_kernel_info(m0: int, m1: int, prec: int) -> dict:
     check(load().swdft2d_stream_kernel_info(m0, m1, prec, buf))
     return {"Q": int(buf[0]), "J": 1 << int(buf[0]), "TP1": int(buf[1]), "threads": int(buf[2]),
             "smem_bytes_ldg": int(buf[3]), "NB": int(buf[4]), "tma_input_staging": bool(buf[5])}
+
+
+def raw_stream(device_index: int) -> int:
+    """cudaStream_t (as an int) of torch's current stream on a device, without the
+    Python-side overhead of torch.cuda.current_stream (which dominated a stream push)."""
+    import torch
+
+    get = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if get is not None:
+        return get(device_index)
+    return torch.cuda.current_stream(device_index).cuda_stream

@@ -171,7 +171,7 @@ class SlidingRowStream2D:
         return slab
 
     def _push(self, r, state, p0, slab) -> int:
-        stream = torch.cuda.current_stream().cuda_stream
+        stream = _lib.raw_stream(self._dev_index)
         if state is not None and self._state_rows < p0:
             self._catch_up(p0, state, stream)
         return self._lib.swdft2d_stream_push(
@@ -254,6 +254,8 @@ class SlidingStream1D:
         self.device = torch.device(device) if device is not None else torch.device(
             "cuda", torch.cuda.current_device())
         self._factor = float(core.normalization_factor(spec))
+        self._dev_index = self.device.index if self.device.index is not None else \
+            torch.cuda.current_device()
         self._ring = torch.zeros(2 * self.n, dtype=_RING_DTYPES[self.prec], device=self.device)
         # n <= 64: K2 pushes (the 1D tree is the dim-0 tree of a 1-column 2D stream:
         # m0 = m, m1 = 0, N1 = 1), one launch per sample over the level state
@@ -301,7 +303,7 @@ class SlidingStream1D:
                 _lib.check(self._lib.swdft2d_stream_push(
                     self._sample.data_ptr(), self._code, 1, None, self._state.data_ptr(), self.m,
                     0, self.prec, self._factor, p, out.data_ptr() if out is not None else None,
-                    _lib.KERNEL_AUTO, torch.cuda.current_stream(self.device).cuda_stream))
+                    _lib.KERNEL_AUTO, _lib.raw_stream(self._dev_index)))
             return out
         if p < n - 1:
             return None

@@ -114,12 +114,15 @@ def forward_into(xt: torch.Tensor, m0: int, m1: int, out: torch.Tensor, *, prec:
         raise ValueError(f"out must be a contiguous {_OUT_DTYPES[prec]} tensor of shape {want}")
     if out.device != xt.device:
         raise ValueError("x and out must be on the same device")
-    if stream is None:
-        stream = torch.cuda.current_stream(xt.device)
-    with torch.cuda.device(xt.device):
-        rc = lib.swdft2d_forward(xt.data_ptr(), _IN_CODES[xt.dtype], N0, N1, xt.stride(0), m0, m1,
-                                 prec, float(scale), p0_begin, p0_end, out.data_ptr(),
-                                 _lib.KERNELS[kernel], stream.cuda_stream)
+    dev = xt.device.index
+    sp = stream.cuda_stream if stream is not None else _lib.raw_stream(dev)
+    args = (xt.data_ptr(), _IN_CODES[xt.dtype], N0, N1, xt.stride(0), m0, m1, prec, float(scale),
+            p0_begin, p0_end, out.data_ptr(), _lib.KERNELS[kernel], sp)
+    if torch.cuda.current_device() == dev:
+        rc = lib.swdft2d_forward(*args)
+    else:
+        with torch.cuda.device(dev):
+            rc = lib.swdft2d_forward(*args)
     _lib.check(rc)
     return out
 
