@@ -35,6 +35,12 @@ static thread_local std::string g_last_error;
 // K1 input path: register prefetch (LDG, default) or TMA tile staging (SWDFT2D_TMA=1).
 // Measured on B200 (profiles/TMA_r01.md): the input is ~0.2 % of the traffic and the
 // LDG variant is 3-12 % faster on configs 2-4 and level on config 5.
+// K1 schedule override: SWDFT2D_K1_GUIDED=1 forces the guided schedule, =0 the uniform
+// one; unset = the measured rule in swdft2d_forward
+static const int g_k1_guided = [] {
+    const char *e = std::getenv("SWDFT2D_K1_GUIDED");
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
+}();
 static const bool g_use_tma = [] {
     const char *e = std::getenv("SWDFT2D_TMA");
     return e && e[0] == '1';
@@ -490,9 +496,41 @@ int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t
             if (v > 0) P.RCH = v < rows ? v : rows;
         }
         P.ntiles = P.CB * ((rows + P.RCH - 1) / P.RCH);
+        unsigned long long *ctr = nullptr;
+        // Guided schedule when there are more column blocks than CTA slots (the uniform
+        // chunks then leave a partial last wave: config 4 837 -> 851-857 Gcoef/s) and the
+        // warm-up is short (n0 <= 32; config 5's 63 warm-up rows made its small tail tiles
+        // cost more: 799 -> 787).  Small problems keep the uniform chunks (config 2 would
+        // pay the counter's memset and the smaller first tiles: 687 -> 618).
+        const bool guided = g_k1_guided >= 0 ? g_k1_guided == 1 : (P.CB >= slots && n0 <= 32);
+        if (guided) {
+            // guided self-scheduling: each row chunk is about half of the remaining work
+            // spread over the CTAs, so big tiles (little warm-up) go first and small ones
+            // fill the tail
+            int64_t R = rows, off = 0;
+            int nc = 0;
+            const int64_t cmin = n0 > 8 ? n0 : 8;
+            P.chunk[0] = 0;
+            while (R > 0) {
+                int64_t c = (R * P.CB + 2 * slots - 1) / (2 * slots);
+                if (c > (R + 1) / 2) c = (R + 1) / 2;
+                if (c < cmin) c = cmin;
+                if (c > R || nc == K1_MAX_CHUNKS - 1) c = R;
+                off += c;
+                R -= c;
+                P.chunk[++nc] = off;
+            }
+            P.nchunks = nc;
+            P.ntiles = P.CB * nc;
+            if (cudaMallocAsync((void **)&ctr, sizeof(unsigned long long), st) != cudaSuccess ||
+                cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st) != cudaSuccess)
+                return fail(SWDFT2D_E_NOMEM, "K1 tile counter: %s", cudaGetErrorString(cudaGetLastError()));
+            P.counter = ctr;
+        }
         std::memcpy(P.tw, k1_twiddles(), sizeof P.tw);
         const int64_t grid = P.ntiles < slots ? P.ntiles : slots;
         k1->launch(P, tmap, (int)grid, st);
+        if (ctr) cudaFreeAsync(ctr, st);
     } else {
         if (m0 > SWDFT2D_K0_MAX_M || m1 > SWDFT2D_K0_MAX_M)
             return fail(SWDFT2D_E_UNSUPPORTED, "window 2^%d x 2^%d exceeds the CUDA paths (max 2^%d)",

@@ -150,11 +150,18 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
 #pragma unroll
     for (int q = 0; q < S::RING; ++q) rring[q] = mk<T>(0, 0);
 
-    for (int64_t tile = blockIdx.x; tile < P.ntiles; tile += gridDim.x) {
+    __shared__ int64_t s_next;
+    for (int64_t tile = blockIdx.x; tile < P.ntiles;) {
         const int64_t cb = tile % P.CB, rc = tile / P.CB;
         const int64_t pbase = cb * TP1;
-        const int64_t r0 = P.p0_begin + rc * P.RCH;                // first output row
-        const int64_t r1 = r0 + P.RCH < P.p0_end ? r0 + P.RCH : P.p0_end;
+        int64_t r0, r1;  // output rows [r0, r1)
+        if (P.nchunks > 0) {
+            r0 = P.p0_begin + P.chunk[rc];
+            r1 = P.p0_begin + P.chunk[rc + 1];
+        } else {
+            r0 = P.p0_begin + rc * P.RCH;
+            r1 = r0 + P.RCH < P.p0_end ? r0 + P.RCH : P.p0_end;
+        }
         const int64_t in_end = r1 + n0 - 1;                         // input rows [r0, in_end)
         const int nbatch = (int)((in_end - r0 + NB - 1) / NB);
         const bool col_ok = pbase + pos < P.P1;
@@ -332,6 +339,13 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
                 });
             }
             __syncthreads();
+        }
+        if (P.counter) {  // guided: the next tile from the shared counter (after the first wave)
+            if (tid == 0) s_next = (int64_t)atomicAdd(P.counter, 1ull) + gridDim.x;
+            __syncthreads();
+            tile = s_next;
+        } else {
+            tile += gridDim.x;
         }
     }
 }

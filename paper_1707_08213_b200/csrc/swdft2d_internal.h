@@ -8,7 +8,8 @@
 
 namespace swdft2d {
 
-constexpr int K1_TW_N = 64;    // K1 twiddle table: make_twiddles(64), read at stride 64/n
+constexpr int K1_TW_N = 64;
+constexpr int K1_MAX_CHUNKS = 48;  // guided K1 schedule: row chunks per launch    // K1 twiddle table: make_twiddles(64), read at stride 64/n
 constexpr int K0_TW_N = 1024;  // K0 twiddle table: make_twiddles(1024), in device memory
 
 struct K0Params {
@@ -29,8 +30,14 @@ struct K1Params {
     void *out;
     double scale;
     int64_t CB;      // column blocks of TP1 window positions
-    int64_t RCH;     // window rows per tile
-    int64_t ntiles;  // CB * ceil(rows / RCH)
+    int64_t RCH;     // window rows per tile (uniform chunks, nchunks == 0)
+    int64_t ntiles;  // CB * number of row chunks
+    // guided schedule (nchunks > 0): row chunk c covers window rows
+    // [p0_begin + chunk[c], p0_begin + chunk[c + 1]); tiles past the first wave are
+    // handed out by atomicAdd on *counter (zeroed before the launch)
+    int nchunks;
+    unsigned long long *counter;
+    int64_t chunk[K1_MAX_CHUNKS + 1];
     int sample_bytes;    // bytes per input sample (4, 8, 16)
     int tma_per_sample;  // TMA elements per sample (1, or 2 for complex128)
     int tma_row_bytes;   // bytes of one staged input row (TMA box width, 16-B multiple)
