@@ -41,6 +41,11 @@ static const int g_k1_guided = [] {
     const char *e = std::getenv("SWDFT2D_K1_GUIDED");
     return e ? (e[0] == '1' ? 1 : 0) : -1;
 }();
+// K1 grid experiment: SWDFT2D_K1_ONESHOT=1 launches one CTA per tile (no persistence)
+static const bool g_k1_oneshot = [] {
+    const char *e = std::getenv("SWDFT2D_K1_ONESHOT");
+    return e && e[0] == '1';
+}();
 static const bool g_use_tma = [] {
     const char *e = std::getenv("SWDFT2D_TMA");
     return e && e[0] == '1';
@@ -502,7 +507,7 @@ int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t
         // warm-up is short (n0 <= 32; config 5's 63 warm-up rows made its small tail tiles
         // cost more: 799 -> 787).  Small problems keep the uniform chunks (config 2 would
         // pay the counter's memset and the smaller first tiles: 687 -> 618).
-        const bool guided = g_k1_guided >= 0 ? g_k1_guided == 1 : (P.CB >= slots && n0 <= 32);
+        const bool guided = !g_k1_oneshot && (g_k1_guided >= 0 ? g_k1_guided == 1 : (P.CB >= slots && n0 <= 32));
         if (guided) {
             // guided self-scheduling: each row chunk is about half of the remaining work
             // spread over the CTAs, so big tiles (little warm-up) go first and small ones
@@ -528,7 +533,7 @@ int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t
             P.counter = ctr;
         }
         std::memcpy(P.tw, k1_twiddles(), sizeof P.tw);
-        const int64_t grid = P.ntiles < slots ? P.ntiles : slots;
+        const int64_t grid = (g_k1_oneshot || P.ntiles < slots) ? P.ntiles : slots;
         k1->launch(P, tmap, (int)grid, st);
         if (ctr) cudaFreeAsync(ctr, st);
     } else {

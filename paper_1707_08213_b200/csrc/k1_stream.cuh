@@ -95,6 +95,14 @@ constexpr size_t k1_smem_bytes() {
            sizeof(cplx<T>) * ((size_t)2 * S::D * TP1 * S::n1 + S::NMAX);
 }
 
+template <typename C> __device__ __forceinline__ void k1_store(C *p, C v) {
+#ifdef K1_PLAIN_STORES  // tuning builds: default-policy stores instead of evict-first
+    *p = v;
+#else
+    st_stream(p, v);
+#endif
+}
+
 template <typename T, int M0, int M1, int Q, int TP1, bool EXACT, int MINB = 1, int NBM = 1,
           bool TMA = false>
 __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
@@ -164,8 +172,14 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
         }
         const int64_t in_end = r1 + n0 - 1;                         // input rows [r0, in_end)
         const int nbatch = (int)((in_end - r0 + NB - 1) / NB);
-        const bool col_ok = pbase + pos < P.P1;
-        C *obase = reinterpret_cast<C *>(P.out) + (pbase + pos) * (int64_t)(n0 * n1) + k1;
+        // Output addressing, kept off the per-row critical path: a running pointer to
+        // the output row of tile row `rel` (advanced by one output row per stage-C row;
+        // rows before the first window row are never dereferenced) and int32 bounds for
+        // the rows that emit: rel in [n0 - 1, rel_hi)
+        const int64_t ostride = P.P1 * (int64_t)(n0 * n1);
+        C *orow = reinterpret_cast<C *>(P.out) + (pbase + pos) * (int64_t)(n0 * n1) + k1 +
+                  (r0 - (n0 - 1) - P.p0_begin) * ostride;
+        const int rel_hi = pbase + pos < P.P1 ? (int)(r1 - r0) + n0 - 1 : 0;
 
         // Input samples of this warp's stage-R tasks for one batch, prefetched one
         // batch ahead so the global-load latency hides behind stage C.
@@ -321,21 +335,23 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
                             rring[off + u] = O;
                         });
                     });
-                    // emit window row p0 = r - (n0 - 1)
-                    const int64_t p0 = r0 + rel - (n0 - 1);
-                    if (rel >= n0 - 1 && p0 < r1 && col_ok) {
-                        C *o = obase + (p0 - P.p0_begin) * P.P1 * (int64_t)(n0 * n1);
-                        static_for<S::OUTS>([&](auto uc) {
-                            constexpr int u = decltype(uc)::value;
-                            C val = cur[u];
-                            if (P.apply_scale) val = cscale(val, (T)P.scale);
-#ifdef K1_PLAIN_STORES  // tuning builds: default-policy stores instead of evict-first
-                            o[(j + J * u) * n1] = val;
-#else
-                            st_stream(o + (j + J * u) * n1, val);
-#endif
-                        });
+                    // emit window row p0 = r0 + rel - (n0 - 1); the scale test is a uniform
+                    // branch (predicated multiplies would cost issue slots on every row)
+                    if (rel >= n0 - 1 && rel < rel_hi) {
+                        if (P.apply_scale) {
+                            const T f = (T)P.scale;
+                            static_for<S::OUTS>([&](auto uc) {
+                                constexpr int u = decltype(uc)::value;
+                                k1_store(orow + (j + J * u) * n1, cscale(cur[u], f));
+                            });
+                        } else {
+                            static_for<S::OUTS>([&](auto uc) {
+                                constexpr int u = decltype(uc)::value;
+                                k1_store(orow + (j + J * u) * n1, cur[u]);
+                            });
+                        }
                     }
+                    orow += ostride;
                 });
             }
             __syncthreads();
