@@ -11,6 +11,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <tuple>
 #include <mutex>
 #include <string>
 #include <utility>
@@ -141,6 +142,9 @@ struct DeviceState {
     void *k0_tw64 = nullptr;  // double2[K0_TW_N]
     void *k0_tw32 = nullptr;  // float2[K0_TW_N]
     std::map<const void *, int> occupancy;  // K1 function -> CTAs per SM
+    // K1 uniform row-chunk choice per (rows, column blocks, slots, n0): the cost-model
+    // scan is thousands of 64-bit divisions, too slow to redo on every call
+    std::map<std::tuple<int64_t, int64_t, int64_t, int>, int64_t> rch;
 };
 static std::mutex g_mu;
 static std::map<int, DeviceState> g_dev;
@@ -178,6 +182,15 @@ static int device_state(DeviceState **out) {
         e = cudaDeviceGetAttribute(&st.sms, cudaDevAttrMultiProcessorCount, dev);
         if (e != cudaSuccess)
             return fail(SWDFT2D_E_CUDA, "cudaDeviceGetAttribute: %s", cudaGetErrorString(e));
+        // The stream-ordered allocations (K1's tile counter, the large-window workspace)
+        // come from the device's default pool, whose release threshold is 0: every
+        // synchronize would hand the memory back and the next call re-map it (measured:
+        // +3.6 ms per config-3 call outside CUDA graphs).  Keep up to 1 GiB cached.
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t keep = 1ull << 30;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
     }
     *out = &st;
     return SWDFT2D_OK;
@@ -495,7 +508,16 @@ int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t
         P.CB = (P1 + k1->tp1 - 1) / k1->tp1;
         const int64_t rows = p0_end - p0_begin;
         const int64_t slots = (int64_t)ds->sms * occ;
-        P.RCH = k1_rows_per_tile(rows, P.CB, slots, n0);
+        {
+            std::lock_guard<std::mutex> lk(g_mu);
+            const auto key = std::make_tuple(rows, P.CB, slots, n0);
+            auto it = ds->rch.find(key);
+            if (it == ds->rch.end()) {
+                if (ds->rch.size() > 4096) ds->rch.clear();
+                it = ds->rch.emplace(key, k1_rows_per_tile(rows, P.CB, slots, n0)).first;
+            }
+            P.RCH = it->second;
+        }
         if (const char *e = std::getenv("SWDFT2D_K1_RCH")) {  // tuning override (rows per tile)
             const long long v = std::atoll(e);
             if (v > 0) P.RCH = v < rows ? v : rows;

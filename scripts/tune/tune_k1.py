@@ -88,7 +88,7 @@ def run_variant(lib, v, name, cfg, cache, dev, flush, a):
             e1.record(s)
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1) / 1e3)
-        t = sum(ts) / len(ts)
+        t = sorted(ts)[len(ts) // 2]  # median: single slow reps (clock dips) do not move it
         err = 0.0
         for a0 in range(0, ref.shape[0], 512):
             a1 = min(a0 + 512, ref.shape[0])
@@ -96,6 +96,7 @@ def run_variant(lib, v, name, cfg, cache, dev, flush, a):
             nrm = ref[a0:a1].abs().pow(2).sum((-1, -2)).sqrt().clamp_min(1e-30)
             err = max(err, float((d / nrm).max()))
         print(json.dumps({"variant": name, "config": cfg.name, "ms": t * 1e3,
+                          "ms_min": min(ts) * 1e3, "ms_max": max(ts) * 1e3,
                           "gcoef_s": cfg.coefficients / t / 1e9,
                           "write_gbs": cfg.coefficients * (16 if a.prec else 8) / t / 1e9,
                           "threads": lib.tune_m(v, 2), "smem": lib.tune_m(v, 3),
