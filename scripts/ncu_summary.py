@@ -84,7 +84,7 @@ def traffic_table(paths):
             du = m["gpu__time_duration.sum"]
             rows.append(f"| {name} | {i} | {du * 1e3:.3f} | {alg / 1e9:.3f} | {rd / 1e9:.4f} | "
                         f"{wr / 1e9:.3f} | {(rd + wr) / alg:.4f} | "
-                        f"{m['dram__bytes_write.sum.per_second'] / 1e12:.2f} |")
+                        f"{m.get('dram__bytes_write.sum.per_second', wr / du) / 1e12:.2f} |")
             per_cfg[name] = {"dram_bytes_per_launch": rd + wr, "full_launch_duration_s": du}
     return rows, per_cfg
 
