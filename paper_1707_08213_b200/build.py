@@ -49,12 +49,41 @@ def _stale(target: str, deps) -> bool:
 
 
 def _compile(src: str, defs, obj: str, verbose: bool) -> str:
-    cmd = [NVCC] + CFLAGS + defs + (["-Xptxas", "-v"] if verbose else []) + [
+    # ptxas -v always: its per-kernel register / stack-frame lines are kept next to the
+    # object (_build/<obj>.ptxas) for tests/test_host.py's local-memory check
+    cmd = [NVCC] + CFLAGS + defs + ["-Xptxas", "-v"] + [
         "-c", os.path.join(CSRC, src), "-o", os.path.join(BUILD, obj)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src} {defs}:\n{r.stdout}\n{r.stderr}")
+    with open(os.path.join(BUILD, obj + ".ptxas"), "w") as f:
+        f.write(r.stderr)
     return r.stderr if verbose else ""
+
+
+def kernel_resources(build_dir: str = BUILD) -> dict:
+    """{mangled kernel: (registers, stack_frame_bytes, spill_store_bytes)} from the
+    ptxas -v logs of the last build (empty if there are none)."""
+    import glob
+    import re
+    res = {}
+    for log in glob.glob(os.path.join(build_dir, "*.ptxas")):
+        fn = None
+        stack = spill = 0
+        for line in open(log):
+            m = re.search(r"Compiling entry function '([^']+)'", line)
+            if m:
+                fn = m.group(1)
+                continue
+            m = re.search(r"(\d+) bytes stack frame, (\d+) bytes spill stores", line)
+            if m and fn:
+                stack, spill = int(m.group(1)), int(m.group(2))
+                continue
+            m = re.search(r"Used (\d+) registers", line)
+            if m and fn:
+                res[fn] = (int(m.group(1)), stack, spill)
+                fn = None
+    return res
 
 
 def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -> str:

@@ -197,3 +197,25 @@ def test_c_abi_example_runs(tmp_path):
                        timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "max window-relative error" in r.stdout
+
+
+def test_kernels_keep_their_state_in_registers():
+    """ptxas -v of the last build: no hot-path kernel uses a local-memory stack frame
+    (a forced call or a dynamically indexed array there once made K1 4.6x slower).
+    Known exceptions: the fp64 64x64 K1 (128-register cap at 512 threads), KR/KC's largest
+    fp64/fp32 trees (<= 24 B), and K0, the bring-up kernel with per-thread row arrays."""
+    from paper_1707_08213_b200 import build
+
+    res = build.kernel_resources()
+    if not res:
+        pytest.skip("no ptxas logs (library built elsewhere)")
+    k1 = {k: v for k, v in res.items() if "k1_stream_kernel" in k}
+    assert len(k1) >= 196
+    allowed_k1 = ("k1_stream_kernelIdLi6ELi6E",)
+    for name, (regs, stack, spill) in res.items():
+        if "k0_window_kernel" in name:
+            continue
+        if "k1_stream_kernel" in name and any(a in name for a in allowed_k1):
+            continue
+        limit = 0 if ("k1_stream_kernel" in name or "k2_push" in name) else 24
+        assert stack <= limit, (name, regs, stack, spill)
