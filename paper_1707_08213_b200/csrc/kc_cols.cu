@@ -81,9 +81,13 @@ __device__ __forceinline__ void kc_pass4(const cplx<T> *src, cplx<T> *dst, const
             const int64_t p1 = cc >> P.m1, k1 = cc & (((int64_t)1 << P.m1) - 1);
             C *o_ = static_cast<C *>(P.out) +
                     ((((r0 + p) * P.P1 + p1) * n0 + j) << P.m1) + k1;
+            if (P.apply_scale) {  // uniform branch: no predicated multiplies when unscaled
 #pragma unroll
-            for (int u = 0; u < 4; ++u)
-                st_stream(o_ + ((int64_t)(u * Lt) << P.m1), P.apply_scale ? cscale(o[u], f) : o[u]);
+                for (int u = 0; u < 4; ++u) st_stream(o_ + ((int64_t)(u * Lt) << P.m1), cscale(o[u], f));
+            } else {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) st_stream(o_ + ((int64_t)(u * Lt) << P.m1), o[u]);
+            }
         } else {
 #pragma unroll
             for (int u = 0; u < 4; ++u) dst[(p * 4 * Lt + j + u * Lt) * CW + col] = o[u];

@@ -69,7 +69,7 @@ __device__ __forceinline__ void kr_pass2(const cplx<T> *src, cplx<T> *dst, const
         const C a0 = src[p * Lt + j], a1 = src[(p + s1) * Lt + j];
         C lo = bfly<EXACT>(a0, wa, a1), hi = bfly<EXACT>(a0, wb, a1);
         if constexpr (LAST) {
-            if (P.apply_scale) {
+            if (P.apply_scale) {  // uniform branch: no predicated multiplies when unscaled
                 lo = cscale(lo, f);
                 hi = cscale(hi, f);
             }
@@ -111,13 +111,18 @@ __device__ __forceinline__ void kr_pass4(const cplx<T> *src, cplx<T> *dst, const
         o[1] = bfly<EXACT>(b1, w2[1], c1);
         o[2] = bfly<EXACT>(b0, w2[2], c0);
         o[3] = bfly<EXACT>(b1, w2[3], c1);
+        if constexpr (LAST) {
+            C *d = dst + p * n + j;
+            if (P.apply_scale) {  // uniform branch: no predicated multiplies when unscaled
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            if constexpr (LAST) {
-                st_stream(dst + p * n + j + u * Lt, P.apply_scale ? cscale(o[u], f) : o[u]);
+                for (int u = 0; u < 4; ++u) st_stream(d + u * Lt, cscale(o[u], f));
             } else {
-                dst[p * 4 * Lt + j + u * Lt] = o[u];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) st_stream(d + u * Lt, o[u]);
             }
+        } else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) dst[p * 4 * Lt + j + u * Lt] = o[u];
         }
     }
 }
