@@ -400,13 +400,15 @@ const K1Info *k1_info() {
 struct K1Choice {
     int m0, m1, q, tp1, minb = 1;  // minb: __launch_bounds__ min CTAs per SM (register cap)
 };
-// (4, 4) and (5, 3) re-tuned after the leaner K1 epilogue (profiles/tune_r01_f.jsonl):
-// 32x8 Q=2/TP1=4 1.232 ms vs 1.305 for Q=3/TP1=2 on config 3; 16x16 with a 5-CTA
-// register cap 0.0902 vs 0.0922 ms on config 2 (config 4 level).
+// Re-tuned after the leaner K1 epilogue: the full window sweep of profiles/sweep_r01b.jsonl
+// (every (Q, TP1) around the rule, windows 4..64 x 4..64) and, for configs 2-4,
+// profiles/tune_r01_f.jsonl.  With the cheaper per-row epilogue, 32-row windows prefer
+// Q = 2 over 3 (32x16: 574 -> 865 Gcoef/s, 32x32: 552 -> 860, 32x8 / config 3: 808 -> 857);
+// 16x16 runs with a 5-CTA register cap (config 2 0.0902 vs 0.0922 ms, config 4 level).
 constexpr K1Choice K1_TUNED_FP32[] = {
-    {2, 3, 0, 32}, {3, 2, 0, 64}, {3, 4, 1, 2}, {4, 3, 2, 8}, {4, 4, 2, 2, 5}, {4, 6, 1, 1},
-    {5, 2, 3, 8},  {5, 3, 2, 4},  {5, 4, 3, 2}, {5, 6, 2, 1}, {6, 2, 3, 2},    {6, 3, 3, 2},
-    {6, 4, 3, 1},  {6, 5, 3, 1},
+    {2, 2, 1, 8},  {2, 3, 0, 32}, {3, 2, 2, 8}, {3, 4, 1, 4}, {4, 2, 2, 16}, {4, 3, 2, 8},
+    {4, 4, 2, 2, 5}, {4, 6, 1, 1}, {5, 2, 3, 8}, {5, 3, 2, 4}, {5, 4, 2, 2},  {5, 5, 2, 1},
+    {5, 6, 2, 1},  {6, 2, 3, 2},  {6, 3, 3, 2}, {6, 4, 3, 1}, {6, 5, 3, 1},
 };
 // (A register cap, MINB 4, helped fp64 (4,4) while the input prefetch stalled on its
 // conversion; with raw-bit prefetch the uncapped kernel is faster on config 4:

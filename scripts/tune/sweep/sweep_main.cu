@@ -2,6 +2,9 @@
 // variants (tuning harness, not product code).
 #include "../../../paper_1707_08213_b200/csrc/abi.cu"
 #include "../../../paper_1707_08213_b200/csrc/k0_window.cu"
+#include "../../../paper_1707_08213_b200/csrc/k2_push.cu"
+#include "../../../paper_1707_08213_b200/csrc/kc_cols.cu"
+#include "../../../paper_1707_08213_b200/csrc/kr_rows.cu"
 #include "../tune_common.cuh"
 
 namespace swdft2d {
