@@ -471,13 +471,16 @@ def e2e_host(args, cfg, x_np, dev, spec, odt, out_dev, world=1):
         ok = torch.tensor([float(psutil.virtual_memory().available > 1.25 * world * need)],
                           dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(ok, op=torch.distributed.ReduceOp.MIN)
-        if not ok.item():
-            return {"skipped": f"host RAM < {world} x {need / 1e9:.0f} GB pinned outputs"}
+        full = bool(ok.item())
+    else:
+        full = True
+    if os.environ.get("SWDFT2D_BENCH_E2E_RESIDENT") == "1":  # exercise the fallback (tests)
+        full = False
     x_pin = torch.from_numpy(x_np).pin_memory()
-    host_out = torch.empty(out_dev.shape, dtype=odt, pin_memory=True)
+    host_out = torch.empty(out_dev.shape, dtype=odt, pin_memory=True) if full else None
     stream = torch.cuda.current_stream(dev)
     times = []
-    for i in range(args.warmup + args.e2e_steps):
+    for i in range(args.warmup + args.e2e_steps if full else 0):
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
@@ -489,8 +492,8 @@ def e2e_host(args, cfg, x_np, dev, spec, odt, out_dev, world=1):
         torch.cuda.synchronize()
         if i >= args.warmup:
             times.append(e0.elapsed_time(e1) / 1e3)
-    s = statistics.mean(times)
-    if world > 1:
+    s = statistics.mean(times) if full else 0.0
+    if world > 1 and full:
         tt = torch.tensor([s], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         s = float(tt.item())
@@ -516,16 +519,23 @@ def e2e_host(args, cfg, x_np, dev, spec, odt, out_dev, world=1):
         tt = torch.tensor([r], dtype=torch.float64, device=dev)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
         r = float(tt.item())
+    resident = {"value": world * cfg.coefficients / r, "unit": UNIT, "ms_per_step": r * 1e3,
+                "h2d_bytes_per_step": int(x_pin.numel() * x_pin.element_size()),
+                "d2h_bytes_per_step": int(win.numel() * win.element_size()),
+                "path": "same call, coefficients left in HBM, one window read back"}
+    if not full:
+        # N full pinned outputs do not fit the host: report the resident variant (input
+        # H2D + transform + a D2H read of one window per rank), saying so
+        return dict(resident, steps=len(rtimes),
+                    full_d2h_skipped=f"host RAM < 1.25 x {world} x {need / 1e9:.0f} GB "
+                                     "pinned outputs; value is the resident variant")
     return {"value": world * cfg.coefficients / s, "unit": UNIT,
             "h2d_bytes_per_step": int(x_pin.numel() * x_pin.element_size()),
             "d2h_bytes_per_step": int(host_out.numel() * host_out.element_size()),
             "ms_per_step": s * 1e3, "steps": len(times),
             "path": "tree_swdft_2d(pinned host input, host_out=pinned): strips computed in a "
                     "device ring and copied D2H on 2 copy streams while later strips compute",
-            "resident": {"value": world * cfg.coefficients / r, "unit": UNIT, "ms_per_step": r * 1e3,
-                         "h2d_bytes_per_step": int(x_pin.numel() * x_pin.element_size()),
-                         "d2h_bytes_per_step": int(win.numel() * win.element_size()),
-                         "path": "same call, coefficients left in HBM, one window read back"}}
+            "resident": resident}
 
 
 def main():

@@ -48,6 +48,18 @@ __global__ void near_persistent(float4 *p, size_t n) {
         for (int u = 0; u < F; ++u) st16(p + base + u * blockDim.x + threadIdx.x, make_float4((float)v, 1.f, (float)u, 3.f));
     }
 }
+// persistent, near pattern, but virtual CTA v is scrambled by an odd-multiplier bijection
+// on [0, nv) (nv a power of two): consecutive steps of one CTA land at unrelated addresses
+template <int F>
+__global__ void near_persistent_scrambled(float4 *p, size_t n) {
+    const size_t nv = n / ((size_t)blockDim.x * F);
+    for (size_t v0 = blockIdx.x; v0 < nv; v0 += gridDim.x) {
+        const size_t v = (v0 * 0x9E3779B1ull) & (nv - 1);
+        const size_t base = v * blockDim.x * F;
+#pragma unroll
+        for (int u = 0; u < F; ++u) st16(p + base + u * blockDim.x + threadIdx.x, make_float4((float)v, 1.f, (float)u, 3.f));
+    }
+}
 // persistent, each CTA owns one contiguous 1/G of the buffer (G fronts as far apart as possible)
 __global__ void own_region(float4 *p, size_t n) {
     const size_t per = n / gridDim.x, b = blockIdx.x * per;
@@ -94,6 +106,15 @@ int main(int argc, char **argv) {
         printf("{\"mode\": \"%s\", \"grid\": %lld, \"threads\": %d, \"GBps\": %.1f}\n", name, grid, threads, bytes / best / 1e6);
         fflush(stdout);
     };
+    if (argc > 1 && argv[1][0] == 's') {
+        for (int occ : {2, 4, 8}) {
+            const int g = sms * occ;
+            timeit("near_persistent_F4", g, 256, [&] { near_persistent<4><<<g, 256>>>(p, n); });
+            timeit("near_persistent_scrambled_F4", g, 256, [&] { near_persistent_scrambled<4><<<g, 256>>>(p, n); });
+            timeit("near_persistent_scrambled_F1", g, 256, [&] { near_persistent_scrambled<1><<<g, 256>>>(p, n); });
+        }
+        return 0;
+    }
     if (argc > 1) return main_waves(p, n, sms, a, b);
     const int T = 256;
     for (int occ : {2, 8}) {
