@@ -410,10 +410,14 @@ constexpr K1Choice K1_TUNED_FP32[] = {
     {4, 4, 2, 2, 5}, {4, 6, 1, 1}, {5, 2, 3, 8}, {5, 3, 2, 4}, {5, 4, 2, 2},  {5, 5, 2, 1},
     {5, 6, 2, 1},  {6, 2, 3, 2},  {6, 3, 3, 2}, {6, 4, 3, 1}, {6, 5, 3, 1},
 };
-// (A register cap, MINB 4, helped fp64 (4,4) while the input prefetch stalled on its
-// conversion; with raw-bit prefetch the uncapped kernel is faster on config 4:
-// 383 vs 368 Gcoef/s, profiles/TUNING_r01.md.)
-constexpr K1Choice K1_TUNED_FP64[] = {{3, 4, 1, 2}};
+// fp64 (exact) from the fp64 window sweep (profiles/sweep64_r01c.jsonl): the rule's
+// choice wherever it is within ~3 % of the best, else the best — e.g. 16x64 292 -> 336,
+// 4x16 320 -> 354 Gcoef/s; 64x64 takes Q = 2 (256 threads, +2 %; like Q = 3 it spills:
+// the fp64 64x64 tree state exceeds the register file at any CTA shape).
+constexpr K1Choice K1_TUNED_FP64[] = {
+    {2, 2, 1, 8}, {2, 3, 0, 8}, {2, 4, 1, 2}, {2, 5, 1, 1}, {2, 6, 0, 1}, {3, 4, 1, 2},
+    {3, 6, 1, 1}, {4, 2, 1, 32}, {4, 6, 1, 1}, {6, 6, 2, 1},
+};
 constexpr int k1_choose_q(int M0, int M1, bool DBL = false) {
     for (const K1Choice &c : K1_TUNED_FP32)
         if (!DBL && c.m0 == M0 && c.m1 == M1) return c.q;
