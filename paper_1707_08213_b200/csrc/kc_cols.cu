@@ -38,16 +38,43 @@ __host__ __device__ constexpr int64_t kc_buf(int M0, int TP0, int which) {
 __host__ __device__ constexpr size_t kc_smem(int M0, int TP0, int CW, int esz) {
     return (size_t)esz * ((size_t)CW * (kc_buf(M0, TP0, 0) + kc_buf(M0, TP0, 1)) + (1u << M0));
 }
-// tile shape: the widest column group (then the most window rows) within the cap
-template <typename T, int M0> struct KCShape {
+// Tile shape (CW columns x TP0 window rows) within the cap, two rules:
+//  * wide (DEEP = false): the widest column group, then the most window rows — long
+//    contiguous Z reads and output runs;
+//  * deep (DEEP = true): the least per-output cost counting the tree nodes the tile
+//    computes (its n0 - 1 halo rows are recomputed, so few window rows cost up to 2x
+//    more butterflies for tall windows), the Z rows it reads, and stores narrower than a
+//    32-byte sector.
+// The output run of a column group is at most n1 columns long (the next columns belong
+// to the next window position), so narrow windows gain nothing from wide groups: the
+// launcher takes the deep rule when n1 x element <= 512 B (measured: 128x8 fp32 3.6 ->
+// 5.0 TB/s, 256x64 3.8 -> 4.0; 128x128 fp64 keeps the wide rule, 4.3 vs 3.9).
+__host__ __device__ constexpr double kc_cost(int M0, int TP0, int CW, int esz) {
+    int64_t nodes = 0;
+    for (int t = 1; t <= M0; ++t) nodes += kc_level_nodes(M0, TP0, t);
+    const double per = (double)TP0 * (double)(1 << M0);
+    const double wide = (double)CW * esz >= 32 ? 1.0 : (double)CW * esz / 32.0;
+    return (double)nodes / per + 2.0 * (double)(TP0 + (1 << M0) - 1) / per + 2.0 / wide;
+}
+template <typename T, int M0, bool DEEP> struct KCShape {
     static constexpr int pick(int what) {
         const int cws[6] = {32, 16, 8, 4, 2, 1};
         const int tps[4] = {16, 8, 4, 2};
+        const int esz = (int)sizeof(T) * 2;
+        int bc = 1, bt = 2;
+        double best = 1e300;
         for (int a = 0; a < 6; ++a)
             for (int b = 0; b < 4; ++b)
-                if (kc_smem(M0, tps[b], cws[a], (int)sizeof(T) * 2) <= KC_SMEM_CAP)
-                    return what == 0 ? cws[a] : tps[b];
-        return 1;
+                if (kc_smem(M0, tps[b], cws[a], esz) <= KC_SMEM_CAP) {
+                    if (!DEEP) return what == 0 ? cws[a] : tps[b];
+                    const double c = kc_cost(M0, tps[b], cws[a], esz);
+                    if (c < best) {
+                        best = c;
+                        bc = cws[a];
+                        bt = tps[b];
+                    }
+                }
+        return what == 0 ? bc : bt;
     }
     static constexpr int CW = pick(0), TP0 = pick(1);
     static constexpr size_t SMEM = kc_smem(M0, TP0, CW, (int)sizeof(T) * 2);
@@ -124,10 +151,10 @@ __device__ __forceinline__ void kc_pass2(const cplx<T> *src, cplx<T> *dst, const
     }
 }
 
-template <typename T, bool EXACT, int M0>
+template <typename T, bool EXACT, int M0, bool DEEP>
 __global__ void __launch_bounds__(KC_THREADS) kc_cols_kernel(const __grid_constant__ KCParams P) {
     using C = cplx<T>;
-    using S = KCShape<T, M0>;
+    using S = KCShape<T, M0, DEEP>;
     constexpr int n0 = 1 << M0, TP0 = S::TP0, CW = S::CW;
     constexpr int W = TP0 + n0 - 1;
     extern __shared__ __align__(16) unsigned char kc_smem_raw[];
@@ -209,10 +236,10 @@ __global__ void __launch_bounds__(KC_THREADS) kc_cols_kernel(const __grid_consta
     }
 }
 
-template <typename T, bool EXACT, int M0>
-static int kc_launch_t(const KCParams &P, cudaStream_t st, int64_t *rows_per_strip_hint) {
-    using S = KCShape<T, M0>;
-    auto fn = &kc_cols_kernel<T, EXACT, M0>;
+template <typename T, bool EXACT, int M0, bool DEEP>
+static int kc_launch_one(const KCParams &P, cudaStream_t st, int64_t *rows_per_strip_hint) {
+    using S = KCShape<T, M0, DEEP>;
+    auto fn = &kc_cols_kernel<T, EXACT, M0, DEEP>;
     if (S::SMEM > 48 * 1024 &&
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM) !=
             cudaSuccess)
@@ -227,6 +254,14 @@ static int kc_launch_t(const KCParams &P, cudaStream_t st, int64_t *rows_per_str
     const int64_t slots = (int64_t)P.sms * occ;
     fn<<<(unsigned)(tiles < slots ? tiles : slots), KC_THREADS, S::SMEM, st>>>(P);
     return 0;
+}
+
+template <typename T, bool EXACT, int M0>
+static int kc_launch_t(const KCParams &P, cudaStream_t st, int64_t *rows_per_strip_hint) {
+    // deep tiles when a window position's n1 columns are a short run (<= 512 B)
+    const bool deep = ((int64_t)sizeof(cplx<T>) << P.m1) <= 512;
+    return deep ? kc_launch_one<T, EXACT, M0, true>(P, st, rows_per_strip_hint)
+                : kc_launch_one<T, EXACT, M0, false>(P, st, rows_per_strip_hint);
 }
 
 template <typename T, bool EXACT>
