@@ -486,3 +486,18 @@ def test_every_k1_window_fp64_bitwise_fp32_tol(cuda, oracle_lib, m0):
         kern = "stream" if m0 > 0 else "rows"
         assert bits_equal(run(x, m0, m1, "fp64", kernel=kern), ref), (m0, m1)
         assert rel_err(run(x.astype(np.complex64), m0, m1, "fp32", kernel=kern), ref) <= FP32_TOL
+
+
+@pytest.mark.parametrize("m,extra", [((9, 2), 40), ((7, 3), 50), ((10, 1), 20)])
+def test_separable_deep_tiles_many_rows(cuda, oracle_lib, m, extra):
+    """KC's deep tile rule (short output runs: n1 x element <= 512 B) with more window rows
+    than one tile holds (TP0 = 16, a partial last tile), including the 227 KB tiles of
+    n0 >= 512 windows: bitwise vs the oracle in fp64, fp32 in tolerance."""
+    m0, m1 = m
+    n0, n1 = 1 << m0, 1 << m1
+    rng = np.random.default_rng(100 + m0)
+    N0, N1 = n0 + extra, n1 + 37
+    x = rng.standard_normal((N0, N1))
+    ref = oracle_lib.tree2d(x, m0, m1)
+    assert bits_equal(run(x, m0, m1, "fp64"), ref)
+    assert rel_err(run(x.astype(np.float32), m0, m1, "fp32"), ref) <= FP32_TOL
