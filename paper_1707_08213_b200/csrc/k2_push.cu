@@ -4,10 +4,10 @@
 // The reference's stream keeps tree levels between pushes so that a push costs
 // O(n0 n1) per window position instead of re-running the window.  K2 does the same
 // on the device, one thread per output column c = (p1, k1), P1 * n1 threads:
-//   1. stage R for the pushed row r alone: Z[r][p1][k1], the node chain of the dim-1
-//      tree that ends in output k1 (n1 - 1 butterflies, the reference's DAG:
-//      level t, shift s_t = n1 >> t, node k1 mod 2^t, twiddle Omega1[(k1 mod 2^t) s_t],
-//      tree2d.py:72-93);
+//   1. stage R for the pushed row r alone: Z[r][p1][k1], the dim-1 tree of each window
+//      position (the reference's DAG, tree2d.py:72-93: level t, shift s_t = n1 >> t,
+//      node k1 mod 2^t, twiddle Omega1[(k1 mod 2^t) s_t]), built cooperatively by the
+//      CTA in shared memory, one level per step (n1 log2 n1 / n1 butterflies per column);
 //   2. the column levels l = 1..m0 of the dim-0 tree (tree2d.py:96-120):
 //      T_l[r][i] = T_{l-1}[r - s_l][i mod h] (+) Omega0[i s_l] (x) T_{l-1}[r][i mod h],
 //      s_l = n0 >> l, h = 2^(l-1).  T_{l-1}[r - s_l] comes from a per-level state ring
@@ -33,19 +33,6 @@ namespace swdft2d {
 template <typename T>
 __device__ __forceinline__ cplx<T> tw64(const K2Params &P, int idx) {
     return mk<T>((T)P.tw[idx].x, (T)P.tw[idx].y);
-}
-
-// Node (L, e - A) of the dim-1 tree, evaluated depth-first (registers ~ L complex):
-// node(t, a) = node(t-1, a + (n1 >> t)) (+) w_t (x) node(t-1, a); leaves are x[e - a].
-template <typename T, bool EXACT, int M1, int L, int A>
-__device__ __forceinline__ cplx<T> rnode(const void *row, int in_dtype, int64_t e, const cplx<T> *w) {
-    if constexpr (L == 0) {
-        return load_x<T>(row, in_dtype, e - A);
-    } else {
-        const cplx<T> cu = rnode<T, EXACT, M1, L - 1, A>(row, in_dtype, e, w);
-        const cplx<T> sh = rnode<T, EXACT, M1, L - 1, A + ((1 << M1) >> L)>(row, in_dtype, e, w);
-        return bfly<EXACT>(sh, w[L - 1], cu);
-    }
 }
 
 // State of level l (l = 1..m0): s_l + 1 slots (s_l = n0 >> l) of 2^(l-1) nodes of
@@ -80,21 +67,52 @@ __global__ void __launch_bounds__(256) k2_push_kernel(const __grid_constant__ K2
         ring[slot * P.N1 + c] = v;
         ring[(slot + n0) * P.N1 + c] = v;
     }
+    // 1. stage R for the pushed row: the CTA's 256 columns are 256 / n1 whole window
+    //    positions (n1 <= 64 divides 256), whose n1-point trees it builds cooperatively in
+    //    shared memory, one tree level per step (every node once, instead of each thread
+    //    re-evaluating the 2^m1-leaf chain of its own output — 63 butterflies and 64
+    //    loads per thread for n1 = 64, times J residue threads).  The nodes and their
+    //    operand roles are the reference DAG's (tree2d.py:72-93), as in rnode:
+    //      Y_t[a][r] = Y_{t-1}[a + (n1 >> t)][r mod 2^(t-1)] (+) Omega1[r (n1 >> t)] (x)
+    //                  Y_{t-1}[a][r mod 2^(t-1)],   a < n1 >> t, r < 2^t,
+    //    Y_0[a][0] = x[e - a] (e = the position's last sample), Z[k1] = Y_m1[0][k1].
+    constexpr int NPOS = 256 / n1;
+    __shared__ C samp[NPOS + n1 - 1];
+    __shared__ C ybuf[2][256];
+    const int64_t cb0 = blockIdx.x * (int64_t)blockDim.x;
+    const int64_t pos0 = cb0 >> M1;
+    if constexpr (M1 > 0) {
+        for (int i = threadIdx.x; i < NPOS + n1 - 1; i += blockDim.x) {
+            const int64_t xi = pos0 + i;
+            samp[i] = xi < P.N1 ? load_x<T>(P.row, P.in_dtype, xi) : mk<T>((T)0, (T)0);
+        }
+        __syncthreads();
+        const int lp = threadIdx.x >> M1, idx = threadIdx.x & (n1 - 1);  // (position, node)
+        static_for<M1>([&](auto tc) {
+            constexpr int t = decltype(tc)::value + 1;
+            constexpr int sa = n1 >> t, hr = 1 << (t - 1);
+            const int a = idx >> t, r = idx & ((1 << t) - 1), rh = r & (hr - 1);
+            C sh, cu;
+            if constexpr (t == 1) {  // level-0 operands straight from the samples
+                sh = samp[lp + n1 - 1 - (a + sa)];
+                cu = samp[lp + n1 - 1 - a];
+            } else {
+                const C *src = ybuf[(t - 2) & 1] + lp * n1;
+                sh = src[(a + sa) * hr + rh];
+                cu = src[a * hr + rh];
+            }
+            ybuf[(t - 1) & 1][lp * n1 + idx] = bfly<EXACT>(sh, stw[r << (6 - t)], cu);
+            __syncthreads();
+        });
+    }
     if (c >= cols) return;
     const int64_t p1 = c >> M1;
     const int k1 = (int)(c & (n1 - 1));
-
-    // 1. stage R: node k1 of the dim-1 tree at end position e = p1 + n1 - 1
     C z;
     if constexpr (M1 == 0) {
         z = load_x<T>(P.row, P.in_dtype, p1);
     } else {
-        C w[M1];  // level-t twiddle of node k1 mod 2^t: Omega1[(k1 mod 2^t) (n1 >> t)]
-        static_for<M1>([&](auto tc) {
-            constexpr int lt = decltype(tc)::value + 1;
-            w[lt - 1] = stw[(k1 & ((1 << lt) - 1)) << (6 - lt)];
-        });
-        z = rnode<T, EXACT, M1, M1, 0>(P.row, P.in_dtype, p1 + n1 - 1, w);
+        z = ybuf[(M1 - 1) & 1][threadIdx.x];
     }
 
     C *__restrict__ out = static_cast<C *>(P.out);
