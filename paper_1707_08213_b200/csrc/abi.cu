@@ -42,10 +42,12 @@ static const int g_k1_guided = [] {
     const char *e = std::getenv("SWDFT2D_K1_GUIDED");
     return e ? (e[0] == '1' ? 1 : 0) : -1;
 }();
-// K1 grid experiment: SWDFT2D_K1_ONESHOT=1 launches one CTA per tile (no persistence)
-static const bool g_k1_oneshot = [] {
+// K1 grid: SWDFT2D_K1_ONESHOT=1 forces one CTA per tile (no persistence), =0 never;
+// unset = the measured rule in swdft2d_forward (one-shot full-height tiles for 64-row
+// windows with several waves of column blocks)
+static const int g_k1_oneshot = [] {
     const char *e = std::getenv("SWDFT2D_K1_ONESHOT");
-    return e && e[0] == '1';
+    return e ? (e[0] == '1' ? 1 : 0) : -1;
 }();
 static const bool g_use_tma = [] {
     const char *e = std::getenv("SWDFT2D_TMA");
@@ -518,6 +520,14 @@ int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t
             }
             P.RCH = it->second;
         }
+        // One-shot grid of full-height tiles (one CTA per column block, scheduled by the
+        // hardware) for 64-row windows when the column blocks fill >= 3 waves: their 63
+        // warm-up rows make short tiles expensive, and short-lived CTAs write faster than
+        // a persistent grid (profiles/write_probe3_r01.jsonl).  Config 5: 804-810 ->
+        // 825-841 Gcoef/s over three alternations (profiles/k1_oneshot_r01.jsonl).  For
+        // n0 <= 32 the gain was within noise (config 4 +0-1.5 %), so they stay persistent.
+        const bool oneshot = g_k1_oneshot >= 0 ? g_k1_oneshot == 1 : (n0 >= 64 && P.CB >= 3 * slots);
+        if (oneshot && g_k1_oneshot < 0) P.RCH = rows;
         if (const char *e = std::getenv("SWDFT2D_K1_RCH")) {  // tuning override (rows per tile)
             const long long v = std::atoll(e);
             if (v > 0) P.RCH = v < rows ? v : rows;
@@ -529,7 +539,7 @@ int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t
         // warm-up is short (n0 <= 32; config 5's 63 warm-up rows made its small tail tiles
         // cost more: 799 -> 787).  Small problems keep the uniform chunks (config 2 would
         // pay the counter's memset and the smaller first tiles: 687 -> 618).
-        const bool guided = !g_k1_oneshot && (g_k1_guided >= 0 ? g_k1_guided == 1 : (P.CB >= slots && n0 <= 32));
+        const bool guided = !oneshot && (g_k1_guided >= 0 ? g_k1_guided == 1 : (P.CB >= slots && n0 <= 32));
         if (guided) {
             // guided self-scheduling: each row chunk is about half of the remaining work
             // spread over the CTAs, so big tiles (little warm-up) go first and small ones
@@ -555,7 +565,7 @@ int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t
             P.counter = ctr;
         }
         std::memcpy(P.tw, k1_twiddles(), sizeof P.tw);
-        const int64_t grid = (g_k1_oneshot || P.ntiles < slots) ? P.ntiles : slots;
+        const int64_t grid = (oneshot || P.ntiles < slots) ? P.ntiles : slots;
         k1->launch(P, tmap, (int)grid, st);
         if (ctr) cudaFreeAsync(ctr, st);
     } else {
