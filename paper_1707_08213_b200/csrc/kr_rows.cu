@@ -14,6 +14,7 @@
 // output, TPOS x n contiguous coefficients per tile (streaming stores).  The
 // same IEEE operation per node as core.butterfly, so fp64 is bitwise equal to the
 // reference.  Per coefficient: ~2 + log2(n)/TPOS butterflies; bound by the writes.
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <utility>
@@ -234,7 +235,20 @@ static int kr_launch_t(const KRParams &P, cudaStream_t st) {
     const int occ = kr_occupancy((const void *)fn, smem);
     if (occ < 1) return -2;
     const int64_t slots = (int64_t)P.sms * occ;
-    fn<<<(unsigned)(tiles < slots ? tiles : slots), KR_THREADS, smem, st>>>(P);
+    // One CTA per tile (hardware-scheduled, short-lived CTAs) when the tiles fill >= 3
+    // waves and the window is <= 256: n = 64..256 write at 6.8-7.2 TB/s instead of
+    // 5.9-6.4 as a persistent grid (fp32; fp64 6.4-7.1 vs 5.9-6.4), n = 16 +2 %.  Windows
+    // of 512-1024 keep the persistent grid: their tiles are 16-32 positions with a
+    // 511-1023-sample halo, which the persistent grid prefetches behind the previous tile
+    // (one-shot: n = 1024 5.56 -> 4.82 TB/s).  profiles/bench_1d_r01.jsonl.
+    // SWDFT2D_KR_ONESHOT=0/1 forces either grid.
+    static const int force = [] {
+        const char *e = std::getenv("SWDFT2D_KR_ONESHOT");
+        return e ? (e[0] == '1' ? 1 : 0) : -1;
+    }();
+    const bool oneshot = force >= 0 ? force == 1 : (M1 <= 8 && tiles >= 3 * slots);
+    const int64_t grid = (oneshot || tiles < slots) ? tiles : slots;
+    fn<<<(unsigned)grid, KR_THREADS, smem, st>>>(P);
     return 0;
 }
 
