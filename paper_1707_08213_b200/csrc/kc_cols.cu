@@ -9,6 +9,8 @@
 // registers; one radix-2 pass first when m0 is odd) with a column dimension: a CTA
 // owns CW consecutive columns (the fast index, so Z reads and output writes are
 // CW-element runs) x TP0 window rows.
+#include <cstdlib>
+
 #include "swdft2d_device.cuh"
 #include "swdft2d_internal.h"
 
@@ -255,7 +257,20 @@ static int kc_launch_one(const KCParams &P, cudaStream_t st, int64_t *rows_per_s
     const int64_t tiles = ((P.cols + S::CW - 1) / S::CW) * ((P.P0s + S::TP0 - 1) / S::TP0);
     if (tiles == 0) return 0;
     const int64_t slots = (int64_t)P.sms * occ;
-    fn<<<(unsigned)(tiles < slots ? tiles : slots), KC_THREADS, S::SMEM, st>>>(P);
+    static const int force = [] {  // SWDFT2D_KC_ONESHOT=0/1: persistent / one CTA per tile
+        const char *e = std::getenv("SWDFT2D_KC_ONESHOT");
+        return e ? (e[0] == '1' ? 1 : 0) : -1;
+    }();
+    // One CTA per tile for deep tiles (short output runs) below the 227 KB shapes, when the
+    // tiles fill >= 3 waves: 128x8 5.0 -> 5.4 TB/s (fp64 5.1 -> 5.7), 256x64 4.0 -> 4.2,
+    // 16x16 forced separable 4.6 -> 5.4; wide tiles lose with it (128x128 fp32 -6 %,
+    // 64x256 -3 %: their persistent grid prefetches the next tile's Z rows), and so do the
+    // one-CTA-per-SM 227 KB tiles of n0 >= 512 (-5 %), and the small trees (n0 <= 8) of the
+    // kD path's dim-0 pass (3-D 4x8x8 -11 %, 8x8x8 -4 %; 16x8x4 gains 9-13 %).
+    // profiles/bench_large_r01b.jsonl, bench_kd_r01b.jsonl.
+    const bool oneshot =
+        force >= 0 ? force == 1 : (DEEP && M0 >= 4 && M0 < 9 && tiles >= 3 * slots);
+    fn<<<(unsigned)((oneshot || tiles < slots) ? tiles : slots), KC_THREADS, S::SMEM, st>>>(P);
     return 0;
 }
 
