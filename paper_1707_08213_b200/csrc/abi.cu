@@ -539,7 +539,10 @@ int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t
         // warm-up is short (n0 <= 32; config 5's 63 warm-up rows made its small tail tiles
         // cost more: 799 -> 787).  Small problems keep the uniform chunks (config 2 would
         // pay the counter's memset and the smaller first tiles: 687 -> 618).
-        const bool guided = !oneshot && (g_k1_guided >= 0 ? g_k1_guided == 1 : (P.CB >= slots && n0 <= 32));
+        // (one-shot grids take the guided chunk sizes only when both are forced: the
+        // hardware then hands the big-first tiles out in blockIdx order, no counter)
+        const bool guided = oneshot ? (g_k1_oneshot == 1 && g_k1_guided == 1)
+                                    : (g_k1_guided >= 0 ? g_k1_guided == 1 : (P.CB >= slots && n0 <= 32));
         if (guided) {
             // guided self-scheduling: each row chunk is about half of the remaining work
             // spread over the CTAs, so big tiles (little warm-up) go first and small ones
@@ -559,10 +562,11 @@ int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t
             }
             P.nchunks = nc;
             P.ntiles = P.CB * nc;
-            if (cudaMallocAsync((void **)&ctr, sizeof(unsigned long long), st) != cudaSuccess ||
-                cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st) != cudaSuccess)
+            if (!oneshot &&
+                (cudaMallocAsync((void **)&ctr, sizeof(unsigned long long), st) != cudaSuccess ||
+                 cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st) != cudaSuccess))
                 return fail(SWDFT2D_E_NOMEM, "K1 tile counter: %s", cudaGetErrorString(cudaGetLastError()));
-            P.counter = ctr;
+            P.counter = ctr;  // nullptr for a one-shot grid: one tile per CTA
         }
         std::memcpy(P.tw, k1_twiddles(), sizeof P.tw);
         const int64_t grid = (oneshot || P.ntiles < slots) ? P.ntiles : slots;
