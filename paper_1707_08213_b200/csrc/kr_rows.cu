@@ -26,6 +26,12 @@ namespace swdft2d {
 
 // Window positions per tile: ~16 K coefficients per CTA (32 K for fp32 n >= 512), the
 // best of 4 K .. 64 K in the sweep of profiles/kr_sweep_r01.jsonl (n = 16 .. 1024).
+// Position cap: 512 for n <= 16 (one-shot CTAs of 256 positions were too short: n = 16
+// 4.99 -> 5.27 TB/s fp32, 5.53 -> 6.36 fp64; a 1024 cap fell back to 5.04 / 5.91),
+// 256 above (n = 32 fp64 spills at 512)
+#ifndef KR_TPOS_CAP
+#define KR_TPOS_CAP (M1 <= 4 ? 512 : 256)
+#endif
 template <typename T, int M1> __host__ __device__ constexpr int kr_tpos() {
 #if defined(KR_PER32) && defined(KR_PER64)  // tuning builds (scripts/tune/kr)
     const int per = (sizeof(T) == 8 ? KR_PER64 : KR_PER32) >> M1;
@@ -33,7 +39,7 @@ template <typename T, int M1> __host__ __device__ constexpr int kr_tpos() {
     const int per = (sizeof(T) == 4 && M1 >= 9 ? 32768 : 16384) >> M1;
 #endif
     const int lo = sizeof(T) == 8 ? 4 : 8;
-    return per < lo ? lo : per > 256 ? 256 : per;
+    return per < lo ? lo : per > KR_TPOS_CAP ? KR_TPOS_CAP : per;
 }
 // Levels kept in shared memory, in pass order: t = 0, then (odd m) 1, then every second
 // level up to m - 2; they alternate between buffer A (even index in that order) and B.
