@@ -68,7 +68,14 @@ extern "C" {
 #define SWDFT2D_KERNEL_SEPARABLE 5  /* KR (rows) + KC (columns) over a workspace, any n <= 1024 */
 
 /* Largest window exponent handled by K1 / by K0, KR and KR + KC. */
+#ifndef SWDFT2D_K1_MAX_M  /* tuning builds may raise it to try larger K1 windows */
 #define SWDFT2D_K1_MAX_M 6
+#endif
+/* K1 also takes 128-row windows (m0 = 7) of n1 <= 16 in fp32; the stream push (K2) stays
+ * at SWDFT2D_K1_MAX_M. */
+#ifndef SWDFT2D_K1_MAX_M0
+#define SWDFT2D_K1_MAX_M0 7
+#endif
 #define SWDFT2D_K0_MAX_M 10
 
 int swdft2d_abi_version(void);

@@ -21,7 +21,7 @@ CSRC = os.path.join(PKG, "csrc")
 BUILD = os.path.join(PKG, "_build")
 LIB = os.path.join(PKG, "libswdft2d.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-K1_MAX_M = 6
+K1_MAX_M = 6   # K1 windows up to 64 x 64; k1_m0_7 adds 128-row windows of n1 <= 16 (fp32)
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
@@ -31,7 +31,7 @@ CFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
 def _units():
     units = [("abi.cu", [], "abi.o"), ("k0_window.cu", [], "k0_window.o"), ("k2_push.cu", [], "k2_push.o"),
              ("kr_rows.cu", [], "kr_rows.o"), ("kc_cols.cu", [], "kc_cols.o")]
-    for m0 in range(K1_MAX_M + 1):
+    for m0 in range(K1_MAX_M + 2):
         units.append(("k1_inst.cu", [f"-DK1_M0={m0}"], f"k1_m0_{m0}.o"))
     return units
 

@@ -31,6 +31,7 @@ void k1_register_m0_3();
 void k1_register_m0_4();
 void k1_register_m0_5();
 void k1_register_m0_6();
+void k1_register_m0_7();
 
 static thread_local std::string g_last_error;
 // K1 input path: register prefetch (LDG, default) or TMA tile staging (SWDFT2D_TMA=1).
@@ -66,7 +67,7 @@ static int fail(int code, const char *fmt, ...) {
 }
 
 // ---- K1 registry ---------------------------------------------------------
-static const K1Info *g_k1[SWDFT2D_K1_MAX_M + 1][SWDFT2D_K1_MAX_M + 1][2][2];  // [m0][m1][prec][tma]
+static const K1Info *g_k1[SWDFT2D_K1_MAX_M0 + 1][SWDFT2D_K1_MAX_M + 1][2][2];  // [m0][m1][prec][tma]
 
 void register_k1(const K1Info *info) { g_k1[info->m0][info->m1][info->prec][info->tma] = info; }
 
@@ -80,12 +81,13 @@ static void ensure_registered() {
         k1_register_m0_4();
         k1_register_m0_5();
         k1_register_m0_6();
+        k1_register_m0_7();
     });
 }
 
 const K1Info *find_k1(int m0, int m1, int prec, int tma) {
     ensure_registered();
-    if (m0 < 0 || m1 < 0 || m0 > SWDFT2D_K1_MAX_M || m1 > SWDFT2D_K1_MAX_M || prec < 0 ||
+    if (m0 < 0 || m1 < 0 || m0 > SWDFT2D_K1_MAX_M0 || m1 > SWDFT2D_K1_MAX_M || prec < 0 ||
         prec > 1 || tma < 0 || tma > 1)
         return nullptr;
     return g_k1[m0][m1][prec][tma];
@@ -746,7 +748,8 @@ int swdft2d_stream_push(const void *row, int in_dtype, int64_t N1, void *ring, v
         P.ring = ring;
         P.out = p0 >= n0 - 1 ? out : nullptr;
         P.scale = scale;
-        std::memcpy(P.tw, k1_twiddles(), sizeof P.tw);
+        for (int i = 0; i < K2_TW_N; ++i)  // make_twiddles(64) = every other entry of (128), bitwise
+            P.tw[i] = k1_twiddles()[i * (K1_TW_N / K2_TW_N)];
         launch_k2(P, m0, m1, prec, st);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return fail(SWDFT2D_E_CUDA, "K2 push: %s", cudaGetErrorString(e));

@@ -16,6 +16,18 @@ template <int M0, int M1> static void reg_pair() {
     K1Inst<M0, M1, true>::reg();
 }
 
+#if K1_M0 == 7
+// 128-row windows: fp32 only, n1 <= 16 (the tree state of wider ones, or in fp64, would
+// not stay in registers); measured vs the separable KR + KC path: 128x4 6.0 vs 4.3 TB/s,
+// 128x8 6.05 vs 5.3, 128x16 5.9 vs 5.5 (profiles/sweep_m7_r01.jsonl)
+void k1_register_m0_7() {
+    K1Inst<7, 0, false>::reg();
+    K1Inst<7, 1, false>::reg();
+    K1Inst<7, 2, false>::reg();
+    K1Inst<7, 3, false>::reg();
+    K1Inst<7, 4, false>::reg();
+}
+#else
 void SWDFT2D_CAT(k1_register_m0_, K1_M0)() {
     reg_pair<K1_M0, 0>();
     reg_pair<K1_M0, 1>();
@@ -25,5 +37,6 @@ void SWDFT2D_CAT(k1_register_m0_, K1_M0)() {
     reg_pair<K1_M0, 5>();
     reg_pair<K1_M0, 6>();
 }
+#endif
 
 }  // namespace swdft2d

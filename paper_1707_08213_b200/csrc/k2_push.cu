@@ -57,8 +57,8 @@ __global__ void __launch_bounds__(256) k2_push_kernel(const __grid_constant__ K2
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int t = (int)blockIdx.y;  // k0 residue class of this thread
     // twiddles in shared memory: stage R indexes them by the lane's k1 (divergent)
-    __shared__ C stw[K1_TW_N];
-    if (threadIdx.x < K1_TW_N) stw[threadIdx.x] = tw64<T>(P, threadIdx.x);
+    __shared__ C stw[K2_TW_N];
+    if (threadIdx.x < K2_TW_N) stw[threadIdx.x] = tw64<T>(P, threadIdx.x);
     __syncthreads();
     if (P.ring && t == 0 && c < P.N1) {  // raw ring, both copies
         const C v = load_x<T>(P.row, P.in_dtype, c);
