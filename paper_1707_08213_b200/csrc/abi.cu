@@ -163,7 +163,8 @@ static void host_twiddles(int n, double *re, double *im) {
     }
 }
 
-// make_twiddles(64) as double2, computed once (every K1/K2 launch passes it by value)
+// make_twiddles(128) as double2, computed once (every K1 launch passes it by value; K2
+// takes every other entry = make_twiddles(64), bitwise)
 static const double2 *k1_twiddles() {
     static const struct Table {
         double2 t[K1_TW_N];
