@@ -32,6 +32,7 @@ void k1_register_m0_4();
 void k1_register_m0_5();
 void k1_register_m0_6();
 void k1_register_m0_7();
+void k1_register_m0_8();
 
 static thread_local std::string g_last_error;
 // K1 input path: register prefetch (LDG, default) or TMA tile staging (SWDFT2D_TMA=1).
@@ -82,6 +83,7 @@ static void ensure_registered() {
         k1_register_m0_5();
         k1_register_m0_6();
         k1_register_m0_7();
+        k1_register_m0_8();
     });
 }
 
@@ -163,8 +165,8 @@ static void host_twiddles(int n, double *re, double *im) {
     }
 }
 
-// make_twiddles(128) as double2, computed once (every K1 launch passes it by value; K2
-// takes every other entry = make_twiddles(64), bitwise)
+// make_twiddles(256) as double2, computed once (every K1 launch passes it by value; K2
+// takes every fourth entry = make_twiddles(64), bitwise)
 static const double2 *k1_twiddles() {
     static const struct Table {
         double2 t[K1_TW_N];
@@ -749,7 +751,7 @@ int swdft2d_stream_push(const void *row, int in_dtype, int64_t N1, void *ring, v
         P.ring = ring;
         P.out = p0 >= n0 - 1 ? out : nullptr;
         P.scale = scale;
-        for (int i = 0; i < K2_TW_N; ++i)  // make_twiddles(64) = every other entry of (128), bitwise
+        for (int i = 0; i < K2_TW_N; ++i)  // make_twiddles(64) = every fourth entry of (256), bitwise
             P.tw[i] = k1_twiddles()[i * (K1_TW_N / K2_TW_N)];
         launch_k2(P, m0, m1, prec, st);
         cudaError_t e = cudaGetLastError();

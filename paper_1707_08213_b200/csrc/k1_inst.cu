@@ -16,7 +16,16 @@ template <int M0, int M1> static void reg_pair() {
     K1Inst<M0, M1, true>::reg();
 }
 
-#if K1_M0 == 7
+#if K1_M0 == 8
+// 256-row windows: fp32, n1 <= 4, Q = 4 (J = 16: a 32-complex register ring, ~220-237
+// registers): 256x1 4.4 vs 2.9 TB/s on KR + KC, 256x2 4.8 vs 4.1, 256x4 5.4 vs 5.1
+// (profiles/sweep_m7_r01.jsonl)
+void k1_register_m0_8() {
+    K1Inst<8, 0, false>::reg();
+    K1Inst<8, 1, false>::reg();
+    K1Inst<8, 2, false>::reg();
+}
+#elif K1_M0 == 7
 // 128-row windows: fp32 only, n1 <= 16 (the tree state of wider ones, or in fp64, would
 // not stay in registers); measured vs the separable KR + KC path: 128x4 6.0 vs 4.3 TB/s,
 // 128x8 6.05 vs 5.3, 128x16 5.9 vs 5.5 (profiles/sweep_m7_r01.jsonl)

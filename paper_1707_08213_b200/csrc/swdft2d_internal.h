@@ -8,7 +8,7 @@
 
 namespace swdft2d {
 
-constexpr int K1_TW_N = 128;  // make_twiddles(128): K1 windows up to 128 rows
+constexpr int K1_TW_N = 256;  // make_twiddles(256): K1 windows up to 256 rows
 constexpr int K2_TW_N = 64;   // make_twiddles(64): K2 (stream push) windows up to 64
 constexpr int K1_MAX_CHUNKS = 48;  // guided K1 schedule: row chunks per launch    // K1 twiddle table: make_twiddles(64), read at stride 64/n
 constexpr int K0_TW_N = 1024;  // K0 twiddle table: make_twiddles(1024), in device memory

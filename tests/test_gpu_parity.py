@@ -503,18 +503,18 @@ def test_separable_deep_tiles_many_rows(cuda, oracle_lib, m, extra):
     assert rel_err(run(x.astype(np.float32), m0, m1, "fp32"), ref) <= FP32_TOL
 
 
-@pytest.mark.parametrize("m1", [0, 1, 2, 3, 4])
-def test_k1_128_row_windows(cuda, oracle_lib, m1):
+@pytest.mark.parametrize("m0,m1", [(7, 0), (7, 1), (7, 2), (7, 3), (7, 4), (8, 0), (8, 1), (8, 2)])
+def test_k1_128_row_windows(cuda, oracle_lib, m0, m1):
     """K1's 128-row windows (m0 = 7, n1 <= 16, fp32 only; 128-entry twiddle table read at
     stride for every smaller window): within BASELINE's tolerance of the oracle, through
     the stream kernel explicitly and through auto; fp64 of the same window takes the
     separable path and stays bitwise."""
-    n0, n1 = 128, 1 << m1
-    rng = np.random.default_rng(700 + m1)
+    n0, n1 = 1 << m0, 1 << m1
+    rng = np.random.default_rng(100 * m0 + m1)
     N0, N1 = n0 + 37, n1 + 45
     x = rng.standard_normal((N0, N1))
-    ref = oracle_lib.tree2d(x, 7, m1)
-    assert _lib.stream_kernel_info(7, m1, 0)["Q"] == 3
-    assert rel_err(run(x.astype(np.float32), 7, m1, "fp32", kernel="stream"), ref) <= FP32_TOL
-    assert rel_err(run(x.astype(np.float32), 7, m1, "fp32"), ref) <= FP32_TOL
-    assert bits_equal(run(x, 7, m1, "fp64"), ref)
+    ref = oracle_lib.tree2d(x, m0, m1)
+    assert _lib.stream_kernel_info(m0, m1, 0)["Q"] == m0 - 4
+    assert rel_err(run(x.astype(np.float32), m0, m1, "fp32", kernel="stream"), ref) <= FP32_TOL
+    assert rel_err(run(x.astype(np.float32), m0, m1, "fp32"), ref) <= FP32_TOL
+    assert bits_equal(run(x, m0, m1, "fp64"), ref)
