@@ -30,6 +30,9 @@ void k1_register_m0_8() {
 // not stay in registers); measured vs the separable KR + KC path: 128x4 6.0 vs 4.3 TB/s,
 // 128x8 6.05 vs 5.3, 128x16 5.9 vs 5.5 (profiles/sweep_m7_r01.jsonl)
 void k1_register_m0_7() {
+    // fp64 only for 128x1 (Q = 4): 3.9 vs 2.8 TB/s separable; 128x2..128x8 in fp64 were
+    // slower on K1 (3.9 / 4.3 / 5.3 vs 4.2 / 5.2 / 5.7)
+    K1Inst<7, 0, true>::reg();
     K1Inst<7, 0, false>::reg();
     K1Inst<7, 1, false>::reg();
     K1Inst<7, 2, false>::reg();

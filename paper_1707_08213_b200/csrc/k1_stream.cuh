@@ -418,7 +418,7 @@ constexpr K1Choice K1_TUNED_FP32[] = {
 // the fp64 64x64 tree state exceeds the register file at any CTA shape).
 constexpr K1Choice K1_TUNED_FP64[] = {
     {2, 2, 1, 8}, {2, 3, 0, 8}, {2, 4, 1, 2}, {2, 5, 1, 1}, {2, 6, 0, 1}, {3, 4, 1, 2},
-    {3, 6, 1, 1}, {4, 2, 1, 32}, {4, 6, 1, 1}, {6, 6, 2, 1},
+    {3, 6, 1, 1}, {4, 2, 1, 32}, {4, 6, 1, 1}, {6, 6, 2, 1}, {7, 0, 4, 8},
 };
 constexpr int k1_choose_q(int M0, int M1, bool DBL = false) {
     for (const K1Choice &c : K1_TUNED_FP32)
