@@ -23,12 +23,12 @@ template <int M0, int M1> static void reg_pair() {
 void k1_register_m0_8() {
     K1Inst<8, 0, false>::reg();
     K1Inst<8, 1, false>::reg();
-    K1Inst<8, 2, false>::reg();
+    K1Inst<8, 2, false>::reg();  // (256x8 measured level with KR + KC: 5.25 vs 5.33 TB/s)
 }
 #elif K1_M0 == 7
-// 128-row windows: fp32 only, n1 <= 16 (the tree state of wider ones, or in fp64, would
-// not stay in registers); measured vs the separable KR + KC path: 128x4 6.0 vs 4.3 TB/s,
-// 128x8 6.05 vs 5.3, 128x16 5.9 vs 5.5 (profiles/sweep_m7_r01.jsonl)
+// 128-row windows: fp32 n1 <= 32 (128x64 would not keep its tree state in registers at
+// 512 threads); measured vs the separable KR + KC path: 128x4 6.0 vs 4.3 TB/s, 128x8 6.05
+// vs 5.3, 128x16 5.9 vs 5.5, 128x32 6.3 vs 5.5 (profiles/sweep_m7_r01.jsonl)
 void k1_register_m0_7() {
     // fp64 only for 128x1 (Q = 4): 3.9 vs 2.8 TB/s separable; 128x2..128x8 in fp64 were
     // slower on K1 (3.9 / 4.3 / 5.3 vs 4.2 / 5.2 / 5.7)
@@ -38,6 +38,7 @@ void k1_register_m0_7() {
     K1Inst<7, 2, false>::reg();
     K1Inst<7, 3, false>::reg();
     K1Inst<7, 4, false>::reg();
+    K1Inst<7, 5, false>::reg();
 }
 #else
 void SWDFT2D_CAT(k1_register_m0_, K1_M0)() {
