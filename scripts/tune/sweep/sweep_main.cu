@@ -15,6 +15,8 @@ void k1_register_m0_3() {}
 void k1_register_m0_4() {}
 void k1_register_m0_5() {}
 void k1_register_m0_6() {}
+void k1_register_m0_7() {}
+void k1_register_m0_8() {}
 extern const Variant SWEEP_2[], SWEEP_3[], SWEEP_4[], SWEEP_5[], SWEEP_6[], SWEEP_7[], SWEEP64[];
 static const Variant *ALL[] = {SWEEP_2, SWEEP_3, SWEEP_4, SWEEP_5, SWEEP_6, SWEEP_7, SWEEP64};
 static const Variant *nth(int v) {
