@@ -540,10 +540,11 @@ int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t
         P.ntiles = P.CB * ((rows + P.RCH - 1) / P.RCH);
         unsigned long long *ctr = nullptr;
         // Guided schedule when there are more column blocks than CTA slots (the uniform
-        // chunks then leave a partial last wave: config 4 837 -> 851-857 Gcoef/s) and the
-        // warm-up is short (n0 <= 32; config 5's 63 warm-up rows made its small tail tiles
-        // cost more: 799 -> 787).  Small problems keep the uniform chunks (config 2 would
-        // pay the counter's memset and the smaller first tiles: 687 -> 618).
+        // chunks then leave a partial last wave: config 4 837 -> 851-857 Gcoef/s, config 3
+        // 724 -> 853) and n0 <= 32.  64-row windows take the one-shot grid above instead
+        // (config 5: persistent uniform 786, persistent guided 826-828, one-shot 858-865;
+        // profiles/k1_oneshot_r01.jsonl).  Small problems keep the uniform chunks (config 2
+        // would pay the counter's memset and the smaller first tiles: 687 -> 618).
         // (one-shot grids take the guided chunk sizes only when both are forced: the
         // hardware then hands the big-first tiles out in blockIdx order, no counter)
         const bool guided = oneshot ? (g_k1_oneshot == 1 && g_k1_guided == 1)
