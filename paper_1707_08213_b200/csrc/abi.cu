@@ -541,14 +541,18 @@ int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t
         unsigned long long *ctr = nullptr;
         // Guided schedule when there are more column blocks than CTA slots (the uniform
         // chunks then leave a partial last wave: config 4 837 -> 851-857 Gcoef/s, config 3
-        // 724 -> 853) and n0 <= 32.  64-row windows take the one-shot grid above instead
-        // (config 5: persistent uniform 786, persistent guided 826-828, one-shot 858-865;
-        // profiles/k1_oneshot_r01.jsonl).  Small problems keep the uniform chunks (config 2
+        // 724 -> 853, 64x4 / 64x8 / 64x16 on ~8 GB outputs 730-758 -> 817-830) for windows
+        // below 2048 coefficients; the largest (32x64, 64x64: one to two 256-512-thread CTAs
+        // per SM) run 6-9 % slower guided and keep the uniform chunks
+        // (profiles/shape_check_r01d.jsonl).  64-row windows with >= 3 waves of column
+        // blocks take the one-shot grid above instead (config 5: persistent uniform 786,
+        // persistent guided 826-828, one-shot 858-865; profiles/k1_oneshot_r01.jsonl).  Small problems keep the uniform chunks (config 2
         // would pay the counter's memset and the smaller first tiles: 687 -> 618).
         // (one-shot grids take the guided chunk sizes only when both are forced: the
         // hardware then hands the big-first tiles out in blockIdx order, no counter)
         const bool guided = oneshot ? (g_k1_oneshot == 1 && g_k1_guided == 1)
-                                    : (g_k1_guided >= 0 ? g_k1_guided == 1 : (P.CB >= slots && n0 <= 32));
+                                    : (g_k1_guided >= 0 ? g_k1_guided == 1
+                                                        : (P.CB >= slots && (n0 << m1) < 2048));
         if (guided) {
             // guided self-scheduling: each row chunk is about half of the remaining work
             // spread over the CTAs, so big tiles (little warm-up) go first and small ones
