@@ -203,6 +203,13 @@ static int device_state(DeviceState **out) {
     return SWDFT2D_OK;
 }
 
+// Relaxes the calling thread's stream-capture mode for its scope (restores it after).
+struct CaptureModeGuard {
+    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+    CaptureModeGuard() { cudaThreadExchangeStreamCaptureMode(&mode); }
+    ~CaptureModeGuard() { cudaThreadExchangeStreamCaptureMode(&mode); }
+};
+
 static int k0_tables(DeviceState *st, const void **tw64, const void **tw32) {
     std::lock_guard<std::mutex> lk(g_mu);
     if (!st->k0_tw64) {
@@ -214,10 +221,20 @@ static int k0_tables(DeviceState *st, const void **tw64, const void **tw32) {
             h64[i] = make_double2(re[i], im[i]);
             h32[i] = make_float2((float)re[i], (float)im[i]);
         }
+        // The first call may come while the caller's stream is being captured into a CUDA
+        // graph: allocate with the thread's capture mode relaxed and upload on a private
+        // non-blocking stream, so the one-time setup neither joins nor breaks the capture.
+        CaptureModeGuard relaxed;
+        cudaStream_t up = nullptr;
         cudaError_t e = cudaMalloc(&st->k0_tw64, sizeof h64);
         if (e == cudaSuccess) e = cudaMalloc(&st->k0_tw32, sizeof h32);
-        if (e == cudaSuccess) e = cudaMemcpy(st->k0_tw64, h64, sizeof h64, cudaMemcpyHostToDevice);
-        if (e == cudaSuccess) e = cudaMemcpy(st->k0_tw32, h32, sizeof h32, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(st->k0_tw64, h64, sizeof h64, cudaMemcpyHostToDevice, up);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(st->k0_tw32, h32, sizeof h32, cudaMemcpyHostToDevice, up);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(up);
+        if (up) cudaStreamDestroy(up);
         if (e != cudaSuccess) {
             cudaFree(st->k0_tw64);
             cudaFree(st->k0_tw32);
@@ -442,6 +459,11 @@ int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t
     if (kernel < SWDFT2D_KERNEL_AUTO || kernel > SWDFT2D_KERNEL_SEPARABLE)
         return fail(SWDFT2D_E_INVALID_ARG, "unknown kernel code %d", kernel);
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    // While the caller's stream is captured into a CUDA graph, the one-time setup of a
+    // first call (device state, twiddle tables, kernel attributes and occupancy, lazy
+    // module loading) runs with the thread's capture mode relaxed: in the default global
+    // mode those calls invalidated the capture.  The launches themselves are captured.
+    CaptureModeGuard relaxed;
     DeviceState *ds = nullptr;
     if ((rc = device_state(&ds))) return rc;
     const int n0 = 1 << m0;
@@ -578,7 +600,11 @@ int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t
                 return fail(SWDFT2D_E_NOMEM, "K1 tile counter: %s", cudaGetErrorString(cudaGetLastError()));
             P.counter = ctr;  // nullptr for a one-shot grid: one tile per CTA
         }
-        std::memcpy(P.tw, k1_twiddles(), sizeof P.tw);
+        {
+            const void *tw64 = nullptr, *tw32 = nullptr;
+            if ((rc = k0_tables(ds, &tw64, &tw32))) return rc;
+            P.tw = static_cast<const double2 *>(tw64);
+        }
         const int64_t grid = (oneshot || P.ntiles < slots) ? P.ntiles : slots;
         k1->launch(P, tmap, (int)grid, st);
         if (ctr) cudaFreeAsync(ctr, st);

@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int i = tid; i < NMAX; i += S::NT) {
-        const double2 w = P.tw[i * (K1_TW_N / NMAX)];
+        const double2 w = P.tw[i * (K0_TW_N / NMAX)];
         tw[i] = mk<T>((T)w.x, (T)w.y);
     }
     if constexpr (TMA) {

@@ -42,7 +42,10 @@ struct K1Params {
     int sample_bytes;    // bytes per input sample (4, 8, 16)
     int tma_per_sample;  // TMA elements per sample (1, or 2 for complex128)
     int tma_row_bytes;   // bytes of one staged input row (TMA box width, 16-B multiple)
-    double2 tw[K1_TW_N];
+    // device make_twiddles(K0_TW_N) in fp64 (the K0 table), read at stride 1024/NMAX:
+    // bitwise make_twiddles(NMAX); a pointer keeps the launch
+    // parameters small (the by-value 256-entry table was 4 KB per launch)
+    const double2 *tw;
 };
 
 // Static shape of one K1 instantiation (filled by the instantiation units).

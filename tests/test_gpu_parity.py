@@ -4,6 +4,8 @@ and the reference's golden vectors.
 fp64 ("DAG-exact") must be BITWISE equal to the reference.  fp32 must satisfy
 BASELINE.json's tolerance: max_k |a_gpu - a_ref| / ||a_ref window||_2 <= 1e-4.
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -519,3 +521,17 @@ def test_k1_128_row_windows(cuda, oracle_lib, m0, m1):
     assert rel_err(run(x.astype(np.float32), m0, m1, "fp32", kernel="stream"), ref) <= FP32_TOL
     assert rel_err(run(x.astype(np.float32), m0, m1, "fp32"), ref) <= FP32_TOL
     assert bits_equal(run(x, m0, m1, "fp64"), ref)
+
+
+def test_first_call_inside_graph_capture(cuda):
+    """A fresh process whose FIRST library call is captured into a CUDA graph: the one-time
+    setup (device state, twiddle tables, kernel attributes, module loading) must not
+    invalidate the capture, and the replay equals a plain call."""
+    import subprocess
+    import sys
+
+    from conftest import ROOT
+
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "first_capture_check.py")],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert "first-call capture ok True" in r.stdout, r.stdout + r.stderr
