@@ -71,10 +71,11 @@ extern "C" {
 #ifndef SWDFT2D_K1_MAX_M  /* tuning builds may raise it to try larger K1 windows */
 #define SWDFT2D_K1_MAX_M 6
 #endif
-/* K1 also takes, in fp32, 128-row windows (m0 = 7) of n1 <= 32 and 256-row windows
- * (m0 = 8) of n1 <= 4 (fp64: 128x1); the stream push (K2) stays at SWDFT2D_K1_MAX_M. */
+/* K1 also takes, in fp32, 128-row windows (m0 = 7) of n1 <= 32, 256-row windows of
+ * n1 <= 4 and 512-row windows of n1 <= 2 (fp64: 128x1); the stream push (K2) stays at
+ * SWDFT2D_K1_MAX_M. */
 #ifndef SWDFT2D_K1_MAX_M0
-#define SWDFT2D_K1_MAX_M0 8
+#define SWDFT2D_K1_MAX_M0 9
 #endif
 #define SWDFT2D_K0_MAX_M 10
 

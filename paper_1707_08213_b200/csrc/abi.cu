@@ -33,6 +33,7 @@ void k1_register_m0_5();
 void k1_register_m0_6();
 void k1_register_m0_7();
 void k1_register_m0_8();
+void k1_register_m0_9();
 
 static thread_local std::string g_last_error;
 // K1 input path: register prefetch (LDG, default) or TMA tile staging (SWDFT2D_TMA=1).
@@ -84,6 +85,7 @@ static void ensure_registered() {
         k1_register_m0_6();
         k1_register_m0_7();
         k1_register_m0_8();
+        k1_register_m0_9();
     });
 }
 

@@ -16,7 +16,14 @@ template <int M0, int M1> static void reg_pair() {
     K1Inst<M0, M1, true>::reg();
 }
 
-#if K1_M0 == 8
+#if K1_M0 == 9
+// 512-row windows: fp32, n1 <= 2, Q = 5 (a 32-complex register ring again): 512x1 3.7 vs
+// 2.8 TB/s on KR + KC, 512x2 3.9 vs 3.4 (profiles/sweep_m7_r01.jsonl)
+void k1_register_m0_9() {
+    K1Inst<9, 0, false>::reg();
+    K1Inst<9, 1, false>::reg();
+}
+#elif K1_M0 == 8
 // 256-row windows: fp32, n1 <= 4, Q = 4 (J = 16: a 32-complex register ring, ~220-237
 // registers): 256x1 4.4 vs 2.9 TB/s on KR + KC, 256x2 4.8 vs 4.1, 256x4 5.4 vs 5.1
 // (profiles/sweep_m7_r01.jsonl)

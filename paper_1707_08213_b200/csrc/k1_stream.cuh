@@ -410,7 +410,7 @@ constexpr K1Choice K1_TUNED_FP32[] = {
     {2, 2, 1, 8},  {2, 3, 0, 32}, {3, 2, 2, 8}, {3, 4, 1, 4}, {4, 2, 2, 16}, {4, 3, 2, 8},
     {4, 4, 2, 2, 5}, {4, 6, 1, 1}, {5, 2, 3, 8}, {5, 3, 2, 4}, {5, 4, 2, 2},  {5, 5, 2, 1},
     {5, 6, 2, 1},  {6, 2, 3, 2},  {6, 3, 3, 2}, {6, 4, 3, 1}, {6, 5, 3, 1},
-    {8, 0, 4, 8},  {8, 1, 4, 4},  {8, 2, 4, 2},
+    {8, 0, 4, 8},  {8, 1, 4, 4},  {8, 2, 4, 2},  {9, 0, 5, 4},  {9, 1, 5, 2},
 };
 // fp64 (exact) from the fp64 window sweep (profiles/sweep64_r01c.jsonl): the rule's
 // choice wherever it is within ~3 % of the best, else the best — e.g. 16x64 292 -> 336,

@@ -53,7 +53,7 @@ def main():
     for case in range(a.cases):
         u = rng.random()
         big, tall = u < 0.15, 0.15 <= u < 0.25  # tall: K1's 128/256-row windows
-        m0 = int(rng.integers(7, 9)) if tall else int(rng.integers(0, 11 if big else 7))
+        m0 = int(rng.integers(7, 10)) if tall else int(rng.integers(0, 11 if big else 7))
         m1 = int(rng.integers(0, 6)) if tall else int(rng.integers(0, 11 if big else 7))
         n0, n1 = 1 << m0, 1 << m1
         # shape: window + extra, bounded output size
@@ -91,7 +91,7 @@ def main():
         err = np.abs(g32 - ref).max(axis=(-1, -2))
         rel32 = float(np.max(np.where(nrm > 0, err / np.where(nrm > 0, nrm, 1), err)))
         worst32 = max(worst32, rel32)
-        k1_big = (m0 == 7 and m1 <= 5) or (m0 == 8 and m1 <= 2)
+        k1_big = (m0 == 7 and m1 <= 5) or (m0 == 8 and m1 <= 2) or (m0 == 9 and m1 <= 1)
         kind = "KR" if m0 == 0 else ("K1" if max(m0, m1) <= 6 or k1_big else "KR+KC")
         kinds[kind] = kinds.get(kind, 0) + 1
         if not bits_equal(got, ref) or rel32 > 1e-4:

@@ -17,6 +17,7 @@ void k1_register_m0_5() {}
 void k1_register_m0_6() {}
 void k1_register_m0_7() {}
 void k1_register_m0_8() {}
+void k1_register_m0_9() {}
 extern const Variant SWEEP_2[], SWEEP_3[], SWEEP_4[], SWEEP_5[], SWEEP_6[], SWEEP_7[], SWEEP64[];
 static const Variant *ALL[] = {SWEEP_2, SWEEP_3, SWEEP_4, SWEEP_5, SWEEP_6, SWEEP_7, SWEEP64};
 static const Variant *nth(int v) {

@@ -18,6 +18,7 @@ void k1_register_m0_5() {}
 void k1_register_m0_6() {}
 void k1_register_m0_7() {}
 void k1_register_m0_8() {}
+void k1_register_m0_9() {}
 
 struct Variant { const char *name; const K1Info *(*info)(); };
 #define V(T, M0, M1, Q, TP1, MINB, NBM)                                                   \

@@ -506,7 +506,7 @@ def test_separable_deep_tiles_many_rows(cuda, oracle_lib, m, extra):
 
 
 @pytest.mark.parametrize("m0,m1", [(7, 0), (7, 1), (7, 2), (7, 3), (7, 4), (7, 5), (8, 0), (8, 1),
-                                   (8, 2)])
+                                   (8, 2), (9, 0), (9, 1)])
 def test_k1_128_row_windows(cuda, oracle_lib, m0, m1):
     """K1's 128-row windows (m0 = 7, n1 <= 16, fp32 only; 128-entry twiddle table read at
     stride for every smaller window): within BASELINE's tolerance of the oracle, through
