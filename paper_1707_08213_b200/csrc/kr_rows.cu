@@ -24,8 +24,9 @@
 
 namespace swdft2d {
 
-// Window positions per tile: ~16 K coefficients per CTA (32 K for fp32 n >= 512), the
-// best of 4 K .. 64 K in the sweep of profiles/kr_sweep_r01.jsonl (n = 16 .. 1024).
+// Window positions per tile: ~16 K coefficients per CTA (32 K for fp32 n >= 512 and fp64
+// n = 1024), the best of 4 K .. 64 K in the sweep of profiles/kr_sweep_r01.jsonl
+// (n = 16 .. 1024); fp64 n = 1024 with 32 positions instead of 16: 3.95 -> 4.88 TB/s.
 // Position cap: 512 for n <= 16 (one-shot CTAs of 256 positions were too short: n = 16
 // 4.99 -> 5.27 TB/s fp32, 5.53 -> 6.36 fp64; a 1024 cap fell back to 5.04 / 5.91),
 // 256 above (n = 32 fp64 spills at 512)
@@ -36,7 +37,7 @@ template <typename T, int M1> __host__ __device__ constexpr int kr_tpos() {
 #if defined(KR_PER32) && defined(KR_PER64)  // tuning builds (scripts/tune/kr)
     const int per = (sizeof(T) == 8 ? KR_PER64 : KR_PER32) >> M1;
 #else
-    const int per = (sizeof(T) == 4 && M1 >= 9 ? 32768 : 16384) >> M1;
+    const int per = (sizeof(T) == 4 && M1 >= 9 ? 32768 : sizeof(T) == 8 && M1 >= 10 ? 32768 : 16384) >> M1;
 #endif
     const int lo = sizeof(T) == 8 ? 4 : 8;
     return per < lo ? lo : per > KR_TPOS_CAP ? KR_TPOS_CAP : per;
