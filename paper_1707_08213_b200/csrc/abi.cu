@@ -167,19 +167,6 @@ static void host_twiddles(int n, double *re, double *im) {
     }
 }
 
-// make_twiddles(256) as double2, computed once (every K1 launch passes it by value; K2
-// takes every fourth entry = make_twiddles(64), bitwise)
-static const double2 *k1_twiddles() {
-    static const struct Table {
-        double2 t[K1_TW_N];
-        Table() {
-            double re[K1_TW_N], im[K1_TW_N];
-            host_twiddles(K1_TW_N, re, im);
-            for (int i = 0; i < K1_TW_N; ++i) t[i] = make_double2(re[i], im[i]);
-        }
-    } table;
-    return table.t;
-}
 
 static int device_state(DeviceState **out) {
     int dev = 0;
@@ -766,6 +753,7 @@ int swdft2d_stream_push(const void *row, int in_dtype, int64_t N1, void *ring, v
     int rc = swdft2d_output_shape(n0, N1, m0, m1, nullptr, &P1);
     if (rc) return rc;
     if (!row || (!ring && !state)) return fail(SWDFT2D_E_INVALID_ARG, "null device pointer");
+    CaptureModeGuard relaxed;  // first-call setup must not invalidate a graph capture
     DeviceState *ds = nullptr;
     if ((rc = device_state(&ds))) return rc;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -784,8 +772,9 @@ int swdft2d_stream_push(const void *row, int in_dtype, int64_t N1, void *ring, v
         P.ring = ring;
         P.out = p0 >= n0 - 1 ? out : nullptr;
         P.scale = scale;
-        for (int i = 0; i < K2_TW_N; ++i)  // make_twiddles(64) = every fourth entry of (256), bitwise
-            P.tw[i] = k1_twiddles()[i * (K1_TW_N / K2_TW_N)];
+        const void *tw64 = nullptr, *tw32 = nullptr;
+        if ((rc = k0_tables(ds, &tw64, &tw32))) return rc;
+        P.tw = static_cast<const double2 *>(tw64);
         launch_k2(P, m0, m1, prec, st);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return fail(SWDFT2D_E_CUDA, "K2 push: %s", cudaGetErrorString(e));

@@ -32,7 +32,8 @@ namespace swdft2d {
 
 template <typename T>
 __device__ __forceinline__ cplx<T> tw64(const K2Params &P, int idx) {
-    return mk<T>((T)P.tw[idx].x, (T)P.tw[idx].y);
+    const double2 w = P.tw[idx * (K0_TW_N / K2_TW_N)];
+    return mk<T>((T)w.x, (T)w.y);
 }
 
 // State of level l (l = 1..m0): s_l + 1 slots (s_l = n0 >> l) of 2^(l-1) nodes of

@@ -8,7 +8,6 @@
 
 namespace swdft2d {
 
-constexpr int K1_TW_N = 256;  // make_twiddles(256): K1 windows up to 256 rows
 constexpr int K2_TW_N = 64;   // make_twiddles(64): K2 (stream push) windows up to 64
 constexpr int K1_MAX_CHUNKS = 48;  // guided K1 schedule: row chunks per launch    // K1 twiddle table: make_twiddles(64), read at stride 64/n
 constexpr int K0_TW_N = 1024;  // K0 twiddle table: make_twiddles(1024), in device memory
@@ -103,7 +102,8 @@ struct K2Params {
     void *ring;   // optional raw ring [2 n0, N1] (nullptr: not stored)
     void *out;    // optional (P1, n0, n1) slab of window row r - n0 + 1
     double scale;
-    double2 tw[K2_TW_N];
+    const double2 *tw;  // device make_twiddles(K0_TW_N), fp64; K2 reads every 16th entry
+                        // = make_twiddles(64), bitwise (small launch parameters)
 };
 int launch_k2(const K2Params &P, int m0, int m1, int prec, cudaStream_t stream);
 
