@@ -13,8 +13,10 @@
 //
 // CTA = TP1 consecutive window columns x all n1 frequencies k1 x J "k0
 // residue groups".  Thread (k1, j, pos) owns column (pos, k1) and the output
-// frequencies k0 = j + J*u.  A persistent grid walks (column block, row chunk)
-// tiles; each tile is processed in batches of NB input rows:
+// frequencies k0 = j + J*u.  The grid walks (column block, row chunk) tiles —
+// persistent CTAs with uniform or guided (big-first, atomic counter) chunks, or, for
+// 64-row windows with many column blocks, one CTA per full-height column block
+// (abi.cu) — and each tile is processed in batches of NB input rows:
 //   0. input: the batch's NB x (TP1 + n1 - 1) samples arrive either by per-lane
 //      loads issued one batch ahead into registers (default), or (TMA=true) as a
 //      cp.async.bulk.tensor tile in a 4-stage shared-memory ring with mbarriers.
@@ -31,7 +33,9 @@
 //      ring, so each row costs 2(n0/J - 1) butterflies per thread.  The n0/J
 //      finished coefficients are written with streaming (evict-first) stores;
 //      consecutive lanes hold consecutive k1, so each warp store is a
-//      contiguous 256-byte (complex64) run of the [P0, P1, n0, n1] output.
+//      contiguous 256-byte (complex64) run of the [P0, P1, n0, n1] output.  The
+//      output address is a running row pointer and the scale a uniform branch, so a
+//      row's epilogue is a handful of instructions.
 //   4. __syncthreads (ring slots are recycled by the next batch's stage R)
 //
 // EXACT (fp64) instantiations use the reference's operand roles and rounding
