@@ -22,8 +22,10 @@
  *     BASELINE.json tolerance: max |err| / ||window||_2 <= 1e-4.
  *
  * Streams: every launch is stream-ordered on the caller's cudaStream_t (passed
- * as void*); the library allocates no device memory per call (the K0 twiddle
- * table cache is allocated once per device and freed by swdft2d_shutdown).
+ * as void*).  Device memory: the twiddle tables and the guided K1 schedule's tile
+ * counters (one 8-byte slot per stream) are allocated once per device and freed by
+ * swdft2d_shutdown; a forward call allocates nothing, except the large-window path
+ * when the caller gives it no workspace (see swdft2d_forward_ws).
  * Errors: functions return SWDFT2D_OK (0) or a negative code; the message of
  * the last error on the calling thread is swdft2d_last_error().
  */
@@ -116,6 +118,38 @@ int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t
                     int m1, int prec, double scale, int64_t p0_begin, int64_t p0_end, void *out,
                     int kernel, void *stream);
 
+/*
+ * swdft2d_forward with a caller-owned device workspace.  Only the large-window path
+ * (KR + KC: a window side above 64, or SWDFT2D_KERNEL_SEPARABLE) uses one: its stage-R
+ * rows of a strip of window rows.  swdft2d_workspace_bytes gives the size the library
+ * would pick (0 when the selected path needs none); any size of at least n0 stage-R
+ * rows works (smaller = shorter strips).  With workspace == NULL the large-window path
+ * takes its workspace stream-ordered from the device's default pool for the call
+ * (cudaMallocAsync / cudaFreeAsync); every other path allocates nothing per call.
+ */
+int swdft2d_forward_ws(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t ld_x, int m0,
+                       int m1, int prec, double scale, int64_t p0_begin, int64_t p0_end, void *out,
+                       void *workspace, int64_t workspace_bytes, int kernel, void *stream);
+
+/* Workspace bytes swdft2d_forward_ws would use for this call (0: none needed). */
+int swdft2d_workspace_bytes(int64_t N0, int64_t N1, int m0, int m1, int prec, int64_t p0_begin,
+                            int64_t p0_end, int kernel, int64_t *bytes);
+
+/*
+ * The K1 launch schedule swdft2d_forward would use for window rows [p0_begin, p0_end)
+ * on the current device (for tests and tuning; the reference has no equivalent):
+ *   info = {mode (0 uniform row chunks on a persistent grid, 1 guided big-first chunks
+ *           on a persistent grid with a tile counter, 2 one-shot grid: one CTA per tile),
+ *           rows per tile (uniform), row chunks, tiles, grid CTAs, column blocks,
+ *           CTA slots (SMs x occupancy), CTAs per SM}
+ *   bounds[c] (c <= chunks, up to max_bounds entries): first window row of chunk c,
+ *           relative to p0_begin; bounds[chunks] = p0_end - p0_begin.
+ * Honours the SWDFT2D_K1_GUIDED / _ONESHOT / _RCH overrides like the forward call.
+ * SWDFT2D_E_UNSUPPORTED if (m0, m1, prec) has no K1 instantiation.
+ */
+int swdft2d_k1_schedule(int64_t N0, int64_t N1, int m0, int m1, int prec, int64_t p0_begin,
+                        int64_t p0_end, int64_t info[8], int64_t *bounds, int max_bounds);
+
 /* Whether K1 is instantiated for (m0, m1, prec): 1 yes, 0 no. */
 int swdft2d_has_stream_kernel(int m0, int m1, int prec);
 
@@ -148,8 +182,9 @@ int swdft2d_strip_range(int64_t P0, int m0, int rank, int world, int64_t range[4
  * Per slot g >= 1: streams[g] waits for x, copies the strip over NVLink (peer access is
  * enabled on first use; cudaMemcpyDefault), then runs swdft2d_forward on the stage.
  * Slot 0 computes straight from x.  Work later enqueued on streams[0] is ordered after
- * every strip copy, so x may be reused from there.  Nothing is allocated on the device;
- * outputs stay on their devices (no gather, no reduction).
+ * every strip copy, so x may be reused from there.  The library allocates no staging
+ * (the caller's stage buffers; per-slot forwards behave as swdft2d_forward); outputs
+ * stay on their devices (no gather, no reduction).
  */
 int swdft2d_forward_multi(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t ld_x,
                           int m0, int m1, int prec, double scale, int ndev, const int *devs,
@@ -189,7 +224,8 @@ int swdft2d_forward_columns(const void *z, int prec, int64_t N0, int64_t cols, i
                             int m_inner, double scale, int64_t p0_begin, int64_t p0_end, void *out,
                             void *stream);
 
-/* Frees cached per-device state (twiddle tables).  Safe to call twice. */
+/* Frees cached per-device state (twiddle tables, tile counters).  Safe to call twice;
+ * no call may be in flight on any stream. */
 int swdft2d_shutdown(void);
 
 #ifdef __cplusplus

@@ -1,0 +1,125 @@
+"""Reference-side binding: the reference package's own ``swdft.tree2d.tree_swdft_2d``
+served by libswdft2d.so on a B200.
+
+This is the module a ``swdft`` maintainer would add: it keeps the
+reference's entry point, types and exceptions, and swaps only the compute.  After
+
+    import swdft.tree2d
+    import swdft_b200            # this file (integration/ on sys.path)
+    swdft_b200.enable()
+
+a caller of ``swdft.tree2d.tree_swdft_2d(x, spec, ...)`` (``/root/reference/pkg/src/
+swdft/tree2d.py:175-202``) gets:
+  * the reference's validation, in its order and with its exception classes
+    (``swdft.core.ShapeError`` / ``WindowTooLargeError`` via ``spec.check_fits`` /
+    ``ValueError`` for ``loop_order`` / ``swdft.core.BudgetError`` from the reference's
+    own ``check_budget`` on the reference's own byte accounting), run by calling the
+    reference's functions themselves (``tree2d.py:189-196``);
+  * a ``swdft.core.CoefficientArray`` (``core.py:258-285``) whose ``values`` are
+    complex128 ``[P0, P1, n0, n1]``, bitwise equal to the reference (the fp64 kernels
+    compute every node with the reference's rounding, ``core.py:223-246``; the
+    normalization factor is applied per component in the store epilogue, bitwise equal
+    to ``core.normalize``, ``core.py:288-302``), recorded with ``spec.normalization``;
+  * the same ``counter.add_region`` calls as ``_levels_outer`` (``tree2d.py:90-92,
+    115-118``), replayed from the reference's own ``core.shift_schedule``.
+
+``values`` is a numpy array, as the reference returns, unless ``enable(values="device")``
+(then a CUDA tensor stays in HBM; ``CoefficientArray`` accepts it).  ``loop_order`` is
+validated and then has no effect (the reference's two orders are bitwise identical);
+``threads`` is accepted and ignored.  There is no CPU fallback: if libswdft2d.so
+cannot be loaded, ``enable()`` raises ImportError.
+"""
+from __future__ import annotations
+
+import functools
+import os
+import sys
+
+_ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+if _ROOT not in sys.path:
+    sys.path.insert(0, _ROOT)
+
+_STATE = {"orig": None, "values": "numpy", "precision": "fp64", "device": None}
+
+
+def _replay_counter(counter, core, shape, spec) -> None:
+    """The add_region calls of the reference's levels-outer schedule (tree2d.py:90-92,
+    115-118): one per level, region = the level's validity thresholds onward."""
+    N0, N1 = shape
+    for g in core.shift_schedule(spec)[1:]:
+        t0, t1 = g.thresholds
+        counter.add_region((slice(t0, N0), slice(t1, N1)), g.nodes_per_tree,
+                           (N0 - t0) * (N1 - t1))
+
+
+def tree_swdft_2d_b200(x, spec, loop_order: str = "levels-outer", counter=None,
+                       budget: int | None = None, threads: int = 1):
+    """swdft.tree2d.tree_swdft_2d (tree2d.py:175-202) with the compute on the B200."""
+    import numpy as np
+    import torch
+    from swdft import core, tree2d
+
+    from paper_1707_08213_b200 import _lib
+    from paper_1707_08213_b200.tree2d import _IN_CODES, _precision_code, forward_into
+
+    # tree2d.py:189-196, verbatim order, the reference's own checks and exceptions
+    x = np.asarray(x, dtype=np.complex128)
+    if x.ndim != 2 or spec.k != 2:
+        raise core.ShapeError("tree_swdft_2d expects a 2D array and 2D window")
+    spec.check_fits(x.shape)
+    if loop_order not in tree2d.LOOP_ORDERS:
+        raise ValueError(f"loop_order must be one of {tree2d.LOOP_ORDERS}")
+    required = core.lattice_bytes(x.shape, spec) + core.output_bytes(x.shape, spec)
+    core.check_budget(required, budget, what="level buffers + coefficient output")
+
+    m0, m1 = (int(m) for m in spec.exponents)
+    n0, n1 = spec.sizes
+    N0, N1 = x.shape
+    P0, P1 = N0 - n0 + 1, N1 - n1 + 1
+    prec = _precision_code(_STATE["precision"], torch.complex128)
+    dev = _STATE["device"] or torch.device("cuda", torch.cuda.current_device())
+    odt = torch.complex128 if prec == _lib.PREC_FP64 else torch.complex64
+    xd = torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+    assert xd.dtype in _IN_CODES
+    out = torch.empty((P0, P1, n0, n1), dtype=odt, device=dev)
+    forward_into(xd, m0, m1, out, prec=prec, scale=float(core.normalization_factor(spec)))
+    if counter is not None:
+        _replay_counter(counter, core, x.shape, spec)
+    values = out if _STATE["values"] == "device" else out.cpu().numpy()
+    # normalize() would have produced this record: values scaled, mode recorded
+    return core.CoefficientArray(values, x.shape, spec, spec.normalization)
+
+
+def enable(values: str = "numpy", precision: str = "fp64", device=None) -> None:
+    """Route swdft.tree2d.tree_swdft_2d to libswdft2d.so (idempotent).
+
+    values     "numpy" (the reference's return type) or "device" (a CUDA tensor)
+    precision  "fp64" (complex128, bitwise equal to the reference) or "fp32"
+               (complex64, within BASELINE.json's 1e-4 of each window's L2 norm)
+    """
+    if values not in ("numpy", "device"):
+        raise ValueError("values must be 'numpy' or 'device'")
+    if precision not in ("fp64", "fp32"):
+        raise ValueError("precision must be 'fp64' or 'fp32'")
+    from swdft import tree2d
+
+    from paper_1707_08213_b200 import _lib
+
+    _lib.load()  # no CPU fallback: fail here, loudly, if the library is missing
+    _STATE.update(values=values, precision=precision, device=device)
+    if _STATE["orig"] is None:
+        _STATE["orig"] = tree2d.tree_swdft_2d
+        tree2d.tree_swdft_2d = functools.wraps(_STATE["orig"])(tree_swdft_2d_b200)
+
+
+def disable() -> None:
+    """Restore the reference's numpy implementation."""
+    from swdft import tree2d
+
+    if _STATE["orig"] is not None:
+        tree2d.tree_swdft_2d = _STATE["orig"]
+        _STATE["orig"] = None
+
+
+def enabled() -> bool:
+    return _STATE["orig"] is not None

@@ -44,6 +44,11 @@ SIGNATURES = {
     "swdft2d_twiddles": (_int, [_int, ctypes.POINTER(ctypes.c_double)]),
     "swdft2d_forward": (_int, [_vp, _int, _i64, _i64, _i64, _int, _int, _int, _dbl, _i64, _i64,
                                _vp, _int, _vp]),
+    "swdft2d_forward_ws": (_int, [_vp, _int, _i64, _i64, _i64, _int, _int, _int, _dbl, _i64,
+                                  _i64, _vp, _vp, _i64, _int, _vp]),
+    "swdft2d_workspace_bytes": (_int, [_i64, _i64, _int, _int, _int, _i64, _i64, _int, _pi64]),
+    "swdft2d_k1_schedule": (_int, [_i64, _i64, _int, _int, _int, _i64, _i64, _pi64, _pi64,
+                                   _int]),
     "swdft2d_has_stream_kernel": (_int, [_int, _int, _int]),
     "swdft2d_stream_kernel_info": (_int, [_int, _int, _int, _pi64]),
     "swdft2d_strip_range": (_int, [_i64, _int, _int, _int, _pi64]),
@@ -133,6 +138,37 @@ def stream_kernel_info(m0: int, m1: int, prec: int) -> dict:
     check(load().swdft2d_stream_kernel_info(m0, m1, prec, buf))
     return {"Q": int(buf[0]), "J": 1 << int(buf[0]), "TP1": int(buf[1]), "threads": int(buf[2]),
             "smem_bytes_ldg": int(buf[3]), "NB": int(buf[4]), "tma_input_staging": bool(buf[5])}
+
+
+def workspace_bytes(N0: int, N1: int, m0: int, m1: int, prec: int, p0_begin: int, p0_end: int,
+                    kernel: int = KERNEL_AUTO) -> int:
+    """Device workspace swdft2d_forward_ws uses for this call (0: the path needs none)."""
+    v = ctypes.c_int64()
+    check(load().swdft2d_workspace_bytes(N0, N1, m0, m1, prec, p0_begin, p0_end, kernel,
+                                         ctypes.byref(v)))
+    return int(v.value)
+
+
+K1_MODES = {0: "uniform", 1: "guided", 2: "oneshot"}
+
+
+def k1_schedule(N0: int, N1: int, m0: int, m1: int, prec: int, p0_begin: int = 0,
+                p0_end: int | None = None) -> dict:
+    """The K1 launch schedule swdft2d_forward picks on the current device
+    (swdft2d_k1_schedule): mode, rows per tile, chunk row bounds (relative to p0_begin),
+    tiles, grid, column blocks, CTA slots, CTAs per SM."""
+    if p0_end is None:
+        p0_end = N0 - (1 << m0) + 1
+    info = (ctypes.c_int64 * 8)()
+    rows = p0_end - p0_begin
+    cap = rows + 2
+    bounds = (ctypes.c_int64 * cap)()
+    check(load().swdft2d_k1_schedule(N0, N1, m0, m1, prec, p0_begin, p0_end, info, bounds, cap))
+    nch = int(info[2])
+    return {"mode": K1_MODES[int(info[0])], "rows_per_tile": int(info[1]), "chunks": nch,
+            "bounds": [int(bounds[c]) for c in range(nch + 1)], "tiles": int(info[3]),
+            "grid": int(info[4]), "column_blocks": int(info[5]), "slots": int(info[6]),
+            "ctas_per_sm": int(info[7])}
 
 
 def raw_stream(device_index: int) -> int:

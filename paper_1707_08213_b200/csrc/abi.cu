@@ -3,8 +3,10 @@
 // Mirrors the validation, accounting and dispatch the reference does around its
 // compute (tree2d.py:175-202, core.py:116-122, 363-388) and launches K1 (fused
 // streaming tree, k1_stream.cuh) or K0 (per-window DAG, k0_window.cu) on the
-// caller's stream.  No torch types, no host threads, no per-call device
-// allocation.
+// caller's stream.  No torch types, no host threads.  Device memory is allocated
+// once per device (twiddle tables, guided-schedule tile counters) and freed by
+// swdft2d_shutdown; a forward call allocates nothing, except the large-window path's
+// workspace when the caller passes none (swdft2d_forward vs swdft2d_forward_ws).
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -153,6 +155,9 @@ struct DeviceState {
     // K1 uniform row-chunk choice per (rows, column blocks, slots, n0): the cost-model
     // scan is thousands of 64-bit divisions, too slow to redo on every call
     std::map<std::tuple<int64_t, int64_t, int64_t, int>, int64_t> rch;
+    // guided K1 tile counters: blocks of zeroed 8-byte slots, one slot per stream handle
+    std::vector<unsigned long long *> ctr_blocks;
+    std::map<cudaStream_t, unsigned long long *> ctr;
 };
 static std::mutex g_mu;
 static std::map<int, DeviceState> g_dev;
@@ -285,28 +290,49 @@ static int64_t k1_rows_per_tile(int64_t rows, int64_t CB, int64_t slots, int n0)
     return best_rch;
 }
 
+// Window rows per strip of the large-window path: the stage-R rows of R window rows
+// (plus the n0 - 1 halo rows) fill the workspace; ~512 MB when the library chooses.
+static int64_t sep_strip_rows(int64_t zrow, int64_t n0, int64_t rows, int64_t ws_bytes) {
+    int64_t R;
+    if (ws_bytes > 0) {
+        R = ws_bytes / zrow - (n0 - 1);
+    } else {
+        R = ((int64_t)512 << 20) / zrow - (n0 - 1);
+        if (R < 64) R = 64;
+    }
+    return R > rows ? rows : R;
+}
+
 // Large-window path (n0 or n1 above K1's 2^6, up to 2^10): the separable schedule in
 // strips of window rows — KR writes the strip's stage-R rows Z (the dim-1 tree of each
-// input row, unscaled) into a stream-ordered workspace, KC runs the dim-0 trees down
-// Z's columns into the output.  Workspace <= ~512 MB per call (cudaMallocAsync /
-// cudaFreeAsync on the caller's stream, so concurrent streams never share it).
+// input row, unscaled) into a workspace, KC runs the dim-0 trees down Z's columns into
+// the output.  The workspace is the caller's (swdft2d_forward_ws, sized by
+// swdft2d_workspace_bytes; a smaller one just means shorter strips); without one the
+// library takes <= ~512 MB stream-ordered from the device pool for the call
+// (cudaMallocAsync / cudaFreeAsync on the caller's stream).
 static int forward_separable(const void *x, int in_dtype, int64_t N1, int64_t ld_x, int m0,
                              int m1, int prec, double scale, int64_t p0_begin, int64_t p0_end,
-                             void *out, cudaStream_t st, DeviceState *ds, const void *tw) {
+                             void *out, void *ws, int64_t ws_bytes, cudaStream_t st,
+                             DeviceState *ds, const void *tw) {
     const int64_t n0 = (int64_t)1 << m0, n1 = (int64_t)1 << m1;
     const int64_t P1 = N1 - n1 + 1, cols = P1 * n1;
     const int64_t esz = prec == SWDFT2D_PREC_FP64 ? 16 : 8;
     const int64_t rows = p0_end - p0_begin;
     const int64_t zrow = cols * esz;
-    int64_t R = ((int64_t)512 << 20) / zrow - (n0 - 1);
-    if (R < 64) R = 64;
-    if (R > rows) R = rows;
-    void *z = nullptr;
-    cudaError_t e = cudaMallocAsync(&z, (size_t)((R + n0 - 1) * zrow), st);
-    if (e != cudaSuccess)
-        return fail(SWDFT2D_E_NOMEM, "large-window workspace (%lld B): %s",
-                    (long long)((R + n0 - 1) * zrow), cudaGetErrorString(e));
+    const int64_t R = sep_strip_rows(zrow, n0, rows, ws ? ws_bytes : 0);
+    if (R < 1)
+        return fail(SWDFT2D_E_INVALID_ARG,
+                    "workspace of %lld B is below one strip (%lld B = n0 stage-R rows)",
+                    (long long)ws_bytes, (long long)(n0 * zrow));
+    void *z = ws;
+    if (!z) {
+        cudaError_t e = cudaMallocAsync(&z, (size_t)((R + n0 - 1) * zrow), st);
+        if (e != cudaSuccess)
+            return fail(SWDFT2D_E_NOMEM, "large-window workspace (%lld B): %s",
+                        (long long)((R + n0 - 1) * zrow), cudaGetErrorString(e));
+    }
     int rc = SWDFT2D_OK;
+    cudaError_t ce;
     for (int64_t a = p0_begin; a < p0_end && rc == SWDFT2D_OK; a += R) {
         const int64_t b = a + R < p0_end ? a + R : p0_end;
         KRParams r;
@@ -338,11 +364,168 @@ static int forward_separable(const void *x, int in_dtype, int64_t N1, int64_t ld
         c.sms = ds->sms;
         if (launch_kr(r, m1, prec, st) || launch_kc(c, m0, prec, st))
             rc = fail(SWDFT2D_E_CUDA, "large-window launch setup failed (m0=%d m1=%d)", m0, m1);
-        else if ((e = cudaGetLastError()) != cudaSuccess)
-            rc = fail(SWDFT2D_E_CUDA, "large-window kernel launch: %s", cudaGetErrorString(e));
+        else if ((ce = cudaGetLastError()) != cudaSuccess)
+            rc = fail(SWDFT2D_E_CUDA, "large-window kernel launch: %s", cudaGetErrorString(ce));
     }
-    cudaFreeAsync(z, st);
+    if (!ws) cudaFreeAsync(z, st);
     return rc;
+}
+
+// Which kernel family serves (m0, m1, prec, kernel); the error code when none does.
+enum Path { PATH_KR, PATH_SEP, PATH_K1, PATH_K0 };
+
+static int select_path(int m0, int m1, int prec, int kernel, Path *path) {
+    if (kernel < SWDFT2D_KERNEL_AUTO || kernel > SWDFT2D_KERNEL_SEPARABLE)
+        return fail(SWDFT2D_E_INVALID_ARG, "unknown kernel code %d", kernel);
+    if (kernel == SWDFT2D_KERNEL_ROWS && m0 != 0)
+        return fail(SWDFT2D_E_UNSUPPORTED, "the row-tree kernel needs n0 = 1 (m0 = %d)", m0);
+    if ((kernel == SWDFT2D_KERNEL_ROWS || kernel == SWDFT2D_KERNEL_AUTO ||
+         kernel == SWDFT2D_KERNEL_SEPARABLE) && m0 == 0) {
+        if (m1 > SWDFT2D_K0_MAX_M)
+            return fail(SWDFT2D_E_UNSUPPORTED, "window 1 x 2^%d exceeds the CUDA paths (max 2^%d)",
+                        m1, SWDFT2D_K0_MAX_M);
+        *path = PATH_KR;
+        return SWDFT2D_OK;
+    }
+    const K1Info *k1 = find_k1(m0, m1, prec, 0);
+    if ((kernel == SWDFT2D_KERNEL_STREAM || kernel == SWDFT2D_KERNEL_STREAM_TMA) && !k1)
+        return fail(SWDFT2D_E_UNSUPPORTED, "no K1 instantiation for m0=%d m1=%d prec=%d", m0, m1, prec);
+    if (kernel != SWDFT2D_KERNEL_SEPARABLE && kernel != SWDFT2D_KERNEL_WINDOW && k1) {
+        *path = PATH_K1;
+        return SWDFT2D_OK;
+    }
+    if (m0 > SWDFT2D_K0_MAX_M || m1 > SWDFT2D_K0_MAX_M)
+        return fail(SWDFT2D_E_UNSUPPORTED, "window 2^%d x 2^%d exceeds the CUDA paths (max 2^%d)",
+                    m0, m1, SWDFT2D_K0_MAX_M);
+    *path = kernel == SWDFT2D_KERNEL_WINDOW ? PATH_K0 : PATH_SEP;
+    return SWDFT2D_OK;
+}
+
+// The K1 launch schedule of window rows [p0_begin, p0_end) (filled into P: CB, RCH,
+// ntiles, nchunks, chunk[]): uniform row chunks on a persistent grid, guided big-first
+// chunks on a persistent grid with a tile counter, or a one-shot grid (one CTA per tile).
+struct K1Plan {
+    int occ = 0;
+    int64_t slots = 0, grid = 0;
+    bool oneshot = false, guided = false;
+};
+
+static int k1_plan(DeviceState *ds, const K1Info *k1, int64_t P1, int64_t p0_begin,
+                   int64_t p0_end, K1Params *P, K1Plan *pl) {
+    const int n0 = 1 << k1->m0;
+    int rc = k1_occupancy(ds, k1, &pl->occ);
+    if (rc) return rc;
+    P->p0_begin = p0_begin;
+    P->p0_end = p0_end;
+    P->CB = (P1 + k1->tp1 - 1) / k1->tp1;
+    const int64_t rows = p0_end - p0_begin;
+    const int64_t slots = (int64_t)ds->sms * pl->occ;
+    pl->slots = slots;
+    {
+        std::lock_guard<std::mutex> lk(g_mu);
+        const auto key = std::make_tuple(rows, P->CB, slots, n0);
+        auto it = ds->rch.find(key);
+        if (it == ds->rch.end()) {
+            if (ds->rch.size() > 4096) ds->rch.clear();
+            it = ds->rch.emplace(key, k1_rows_per_tile(rows, P->CB, slots, n0)).first;
+        }
+        P->RCH = it->second;
+    }
+    // One-shot grid of full-height tiles (one CTA per column block, scheduled by the
+    // hardware) for 64-row windows when the column blocks fill >= 3 waves: their 63
+    // warm-up rows make short tiles expensive, and short-lived CTAs write faster than
+    // a persistent grid (profiles/write_probe3_r01.jsonl).  Config 5: 804-810 ->
+    // 825-841 Gcoef/s over three alternations (profiles/k1_oneshot_r01.jsonl).  For
+    // n0 <= 32 the gain was within noise (config 4 +0-1.5 %), so they stay persistent.
+    const bool oneshot = g_k1_oneshot >= 0 ? g_k1_oneshot == 1 : (n0 >= 64 && P->CB >= 3 * slots);
+    if (oneshot && g_k1_oneshot < 0) P->RCH = rows;
+    if (const char *e = std::getenv("SWDFT2D_K1_RCH")) {  // tuning / test override (rows per tile)
+        const long long v = std::atoll(e);
+        if (v > 0) P->RCH = v < rows ? v : rows;
+    }
+    P->nchunks = 0;
+    P->ntiles = P->CB * ((rows + P->RCH - 1) / P->RCH);
+    // Guided schedule when there are more column blocks than CTA slots (the uniform
+    // chunks then leave a partial last wave: config 4 837 -> 851-857 Gcoef/s, config 3
+    // 724 -> 853, 64x4 / 64x8 / 64x16 on ~8 GB outputs 730-758 -> 817-830) for windows
+    // below 2048 coefficients; the largest (32x64, 64x64: one to two 256-512-thread CTAs
+    // per SM) run 6-9 % slower guided and keep the uniform chunks
+    // (profiles/shape_check_r01d.jsonl).  64-row windows with >= 3 waves of column
+    // blocks take the one-shot grid above instead (config 5: persistent uniform 786,
+    // persistent guided 826-828, one-shot 858-865; profiles/k1_oneshot_r01.jsonl).  Small
+    // problems keep the uniform chunks (config 2: guided 687 -> 618).
+    // (one-shot grids take the guided chunk sizes only when both are forced: the
+    // hardware then hands the big-first tiles out in blockIdx order, no counter)
+    const bool guided = oneshot ? (g_k1_oneshot == 1 && g_k1_guided == 1)
+                                : (g_k1_guided >= 0 ? g_k1_guided == 1
+                                                    : (P->CB >= slots && (n0 << k1->m1) < 2048));
+    if (guided) {
+        // guided self-scheduling: each row chunk is about half of the remaining work
+        // spread over the CTAs, so big tiles (little warm-up) go first and small ones
+        // fill the tail
+        int64_t R = rows, off = 0;
+        int nc = 0;
+        const int64_t cmin = n0 > 8 ? n0 : 8;
+        P->chunk[0] = 0;
+        while (R > 0) {
+            int64_t c = (R * P->CB + 2 * slots - 1) / (2 * slots);
+            if (c > (R + 1) / 2) c = (R + 1) / 2;
+            if (c < cmin) c = cmin;
+            if (c > R || nc == K1_MAX_CHUNKS - 1) c = R;
+            off += c;
+            R -= c;
+            P->chunk[++nc] = off;
+        }
+        P->nchunks = nc;
+        P->ntiles = P->CB * nc;
+    }
+    pl->oneshot = oneshot;
+    pl->guided = guided;
+    pl->grid = (oneshot || P->ntiles < slots) ? P->ntiles : slots;
+    return SWDFT2D_OK;
+}
+
+// The guided K1 tile counter of (current device, stream): one 8-byte slot per stream
+// handle, from blocks allocated and zeroed once (the kernel leaves it zeroed after every
+// launch), so a forward call allocates nothing.  Launches on one stream are ordered, so
+// they can share the slot; distinct streams never do (up to K1_CTR_MAX streams per device,
+// after which slots are recycled).
+static constexpr int K1_CTR_BLOCK = 256, K1_CTR_MAX = 16 * K1_CTR_BLOCK;
+
+static int k1_counter(DeviceState *ds, cudaStream_t s, unsigned long long **out) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = ds->ctr.find(s);
+    if (it != ds->ctr.end()) {
+        *out = it->second;
+        return SWDFT2D_OK;
+    }
+    const size_t used = ds->ctr.size();
+    if (used >= (size_t)K1_CTR_MAX) {  // recycle: every slot is zero between launches
+        unsigned long long *p = ds->ctr.begin()->second;
+        ds->ctr.erase(ds->ctr.begin());
+        ds->ctr[s] = p;
+        *out = p;
+        return SWDFT2D_OK;
+    }
+    if (used == ds->ctr_blocks.size() * K1_CTR_BLOCK) {
+        CaptureModeGuard relaxed;
+        void *blk = nullptr;
+        cudaStream_t up = nullptr;
+        cudaError_t e = cudaMalloc(&blk, K1_CTR_BLOCK * sizeof(unsigned long long));
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaMemsetAsync(blk, 0, K1_CTR_BLOCK * sizeof(unsigned long long), up);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(up);
+        if (up) cudaStreamDestroy(up);
+        if (e != cudaSuccess) {
+            if (blk) cudaFree(blk);
+            return fail(SWDFT2D_E_NOMEM, "K1 tile counters: %s", cudaGetErrorString(e));
+        }
+        ds->ctr_blocks.push_back(static_cast<unsigned long long *>(blk));
+    }
+    unsigned long long *p = ds->ctr_blocks[used / K1_CTR_BLOCK] + used % K1_CTR_BLOCK;
+    ds->ctr[s] = p;
+    *out = p;
+    return SWDFT2D_OK;
 }
 
 }  // namespace swdft2d
@@ -428,44 +611,108 @@ int swdft2d_strip_range(int64_t P0, int m0, int rank, int world, int64_t range[4
     return SWDFT2D_OK;
 }
 
-int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t ld_x, int m0,
-                    int m1, int prec, double scale, int64_t p0_begin, int64_t p0_end, void *out,
-                    int kernel, void *stream) {
+// Shared validation of swdft2d_forward* / swdft2d_workspace_bytes.
+static int check_forward_args(int in_dtype, int64_t N0, int64_t N1, int64_t ld_x, int m0, int m1,
+                              int prec, int64_t p0_begin, int64_t p0_end, int64_t *P1) {
     if (in_dtype < SWDFT2D_IN_F32 || in_dtype > SWDFT2D_IN_C128)
         return fail(SWDFT2D_E_INVALID_ARG, "unknown input dtype code %d", in_dtype);
     if (prec != SWDFT2D_PREC_FP32 && prec != SWDFT2D_PREC_FP64)
         return fail(SWDFT2D_E_INVALID_ARG, "unknown precision code %d", prec);
     if (N0 < 1 || N1 < 1) return fail(SWDFT2D_E_SHAPE, "empty input (%lld x %lld)", (long long)N0, (long long)N1);
     if (ld_x < N1) return fail(SWDFT2D_E_INVALID_ARG, "ld_x %lld < N1 %lld", (long long)ld_x, (long long)N1);
-    int64_t P0 = 0, P1 = 0;
-    int rc = swdft2d_output_shape(N0, N1, m0, m1, &P0, &P1);
+    int64_t P0 = 0;
+    int rc = swdft2d_output_shape(N0, N1, m0, m1, &P0, P1);
     if (rc) return rc;
     if (p0_begin < 0 || p0_end > P0 || p0_begin > p0_end)
         return fail(SWDFT2D_E_INVALID_ARG, "window rows [%lld, %lld) outside [0, %lld)",
                     (long long)p0_begin, (long long)p0_end, (long long)P0);
-    if (p0_begin == p0_end) return SWDFT2D_OK;
-    if (!x || !out) return fail(SWDFT2D_E_INVALID_ARG, "null device pointer");
-    if (kernel < SWDFT2D_KERNEL_AUTO || kernel > SWDFT2D_KERNEL_SEPARABLE)
-        return fail(SWDFT2D_E_INVALID_ARG, "unknown kernel code %d", kernel);
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    // While the caller's stream is captured into a CUDA graph, the one-time setup of a
-    // first call (device state, twiddle tables, kernel attributes and occupancy, lazy
-    // module loading) runs with the thread's capture mode relaxed: in the default global
-    // mode those calls invalidated the capture.  The launches themselves are captured.
+    return SWDFT2D_OK;
+}
+
+int swdft2d_workspace_bytes(int64_t N0, int64_t N1, int m0, int m1, int prec, int64_t p0_begin,
+                            int64_t p0_end, int kernel, int64_t *bytes) {
+    if (!bytes) return fail(SWDFT2D_E_INVALID_ARG, "null output");
+    int64_t P1 = 0;
+    int rc = check_forward_args(SWDFT2D_IN_F32, N0, N1, N1, m0, m1, prec, p0_begin, p0_end, &P1);
+    if (rc) return rc;
+    Path path;
+    if ((rc = select_path(m0, m1, prec, kernel, &path))) return rc;
+    *bytes = 0;
+    if (path != PATH_SEP || p0_end == p0_begin) return SWDFT2D_OK;
+    const int64_t n0 = (int64_t)1 << m0;
+    const int64_t zrow = P1 * ((int64_t)1 << m1) * (prec == SWDFT2D_PREC_FP64 ? 16 : 8);
+    const int64_t R = sep_strip_rows(zrow, n0, p0_end - p0_begin, 0);
+    *bytes = (R + n0 - 1) * zrow;
+    return SWDFT2D_OK;
+}
+
+int swdft2d_k1_schedule(int64_t N0, int64_t N1, int m0, int m1, int prec, int64_t p0_begin,
+                        int64_t p0_end, int64_t info[8], int64_t *bounds, int max_bounds) {
+    if (!info) return fail(SWDFT2D_E_INVALID_ARG, "null info");
+    int64_t P1 = 0;
+    int rc = check_forward_args(SWDFT2D_IN_F32, N0, N1, N1, m0, m1, prec, p0_begin, p0_end, &P1);
+    if (rc) return rc;
+    const K1Info *k1 = find_k1(m0, m1, prec, 0);
+    if (!k1) return fail(SWDFT2D_E_UNSUPPORTED, "no K1 instantiation for m0=%d m1=%d prec=%d", m0, m1, prec);
+    if (p0_end == p0_begin) return fail(SWDFT2D_E_INVALID_ARG, "empty row range");
     CaptureModeGuard relaxed;
     DeviceState *ds = nullptr;
     if ((rc = device_state(&ds))) return rc;
-    const int n0 = 1 << m0;
+    K1Params P;
+    std::memset(&P, 0, sizeof P);
+    K1Plan pl;
+    if ((rc = k1_plan(ds, k1, P1, p0_begin, p0_end, &P, &pl))) return rc;
+    const int64_t rows = p0_end - p0_begin;
+    const int64_t nchunks = P.nchunks > 0 ? P.nchunks : (rows + P.RCH - 1) / P.RCH;
+    info[0] = pl.oneshot ? 2 : pl.guided ? 1 : 0;
+    info[1] = P.RCH;
+    info[2] = nchunks;
+    info[3] = P.ntiles;
+    info[4] = pl.grid;
+    info[5] = P.CB;
+    info[6] = pl.slots;
+    info[7] = pl.occ;
+    for (int64_t c = 0; bounds && c <= nchunks && c < max_bounds; ++c) {
+        const int64_t v = P.nchunks > 0 ? P.chunk[c] : c * P.RCH;
+        bounds[c] = v < rows ? v : rows;
+    }
+    return SWDFT2D_OK;
+}
+
+int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t ld_x, int m0,
+                    int m1, int prec, double scale, int64_t p0_begin, int64_t p0_end, void *out,
+                    int kernel, void *stream) {
+    return swdft2d_forward_ws(x, in_dtype, N0, N1, ld_x, m0, m1, prec, scale, p0_begin, p0_end,
+                              out, nullptr, 0, kernel, stream);
+}
+
+int swdft2d_forward_ws(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t ld_x, int m0,
+                       int m1, int prec, double scale, int64_t p0_begin, int64_t p0_end, void *out,
+                       void *workspace, int64_t workspace_bytes, int kernel, void *stream) {
+    int64_t P1 = 0;
+    int rc = check_forward_args(in_dtype, N0, N1, ld_x, m0, m1, prec, p0_begin, p0_end, &P1);
+    if (rc) return rc;
+    Path path;
+    if ((rc = select_path(m0, m1, prec, kernel, &path))) return rc;
+    if (p0_begin == p0_end) return SWDFT2D_OK;
+    if (!x || !out) return fail(SWDFT2D_E_INVALID_ARG, "null device pointer");
+    if (workspace_bytes < 0 || (workspace_bytes > 0 && !workspace))
+        return fail(SWDFT2D_E_INVALID_ARG, "bad workspace (%p, %lld B)", workspace,
+                    (long long)workspace_bytes);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    // While the caller's stream is captured into a CUDA graph, the one-time setup of a
+    // first call (device state, twiddle tables, tile counters, kernel attributes and
+    // occupancy, lazy module loading) runs with the thread's capture mode relaxed: in the
+    // default global mode those calls invalidated the capture.  The launches are captured.
+    CaptureModeGuard relaxed;
+    DeviceState *ds = nullptr;
+    if ((rc = device_state(&ds))) return rc;
+    const void *tw64 = nullptr, *tw32 = nullptr;
+    if ((rc = k0_tables(ds, &tw64, &tw32))) return rc;
+    const void *tw = prec == SWDFT2D_PREC_FP64 ? tw64 : tw32;
     const bool apply = !(scale == 1.0);
 
-    if (kernel == SWDFT2D_KERNEL_ROWS && m0 != 0)
-        return fail(SWDFT2D_E_UNSUPPORTED, "the row-tree kernel needs n0 = 1 (m0 = %d)", m0);
-    if ((kernel == SWDFT2D_KERNEL_ROWS || kernel == SWDFT2D_KERNEL_AUTO || kernel == SWDFT2D_KERNEL_SEPARABLE) && m0 == 0) {
-        if (m1 > SWDFT2D_K0_MAX_M)
-            return fail(SWDFT2D_E_UNSUPPORTED, "window 1 x 2^%d exceeds the CUDA paths (max 2^%d)",
-                        m1, SWDFT2D_K0_MAX_M);
-        const void *tw64 = nullptr, *tw32 = nullptr;
-        if ((rc = k0_tables(ds, &tw64, &tw32))) return rc;
+    if (path == PATH_KR) {
         KRParams P;
         std::memset(&P, 0, sizeof P);
         P.x = x;
@@ -478,131 +725,42 @@ int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t
         P.P1 = P1;
         P.out = out;
         P.scale = scale;
-        P.tw = prec == SWDFT2D_PREC_FP64 ? tw64 : tw32;
+        P.tw = tw;
         P.sms = ds->sms;
         const int r = launch_kr(P, m1, prec, st);
         if (r != 0) return fail(SWDFT2D_E_CUDA, "row-tree kernel launch setup failed (%d)", r);
-        cudaError_t e = cudaGetLastError();
-        if (e != cudaSuccess) return fail(SWDFT2D_E_CUDA, "kernel launch: %s", cudaGetErrorString(e));
-        return SWDFT2D_OK;
-    }
-
-    const K1Info *k1 = find_k1(m0, m1, prec, 0);
-    if ((kernel == SWDFT2D_KERNEL_STREAM || kernel == SWDFT2D_KERNEL_STREAM_TMA) && !k1)
-        return fail(SWDFT2D_E_UNSUPPORTED, "no K1 instantiation for m0=%d m1=%d prec=%d", m0, m1, prec);
-    if (kernel == SWDFT2D_KERNEL_SEPARABLE || (kernel == SWDFT2D_KERNEL_AUTO && !k1)) {
-        if (m0 > SWDFT2D_K0_MAX_M || m1 > SWDFT2D_K0_MAX_M)
-            return fail(SWDFT2D_E_UNSUPPORTED, "window 2^%d x 2^%d exceeds the CUDA paths (max 2^%d)",
-                        m0, m1, SWDFT2D_K0_MAX_M);
-        const void *tw64 = nullptr, *tw32 = nullptr;
-        if ((rc = k0_tables(ds, &tw64, &tw32))) return rc;
-        return forward_separable(x, in_dtype, N1, ld_x, m0, m1, prec, scale, p0_begin, p0_end, out,
-                                 st, ds, prec == SWDFT2D_PREC_FP64 ? tw64 : tw32);
-    }
-    if (kernel != SWDFT2D_KERNEL_WINDOW && k1) {
+    } else if (path == PATH_SEP) {
+        if ((rc = forward_separable(x, in_dtype, N1, ld_x, m0, m1, prec, scale, p0_begin, p0_end,
+                                    out, workspace, workspace_bytes, st, ds, tw)))
+            return rc;
+    } else if (path == PATH_K1) {
+        const K1Info *k1 = find_k1(m0, m1, prec, 0);
         K1Params P;
         std::memset(&P, 0, sizeof P);
         CUtensorMap tmap;
         std::memset(&tmap, 0, sizeof tmap);
-        // the TMA variant stages input tiles with cp.async.bulk.tensor when x is addressable
+        // the TMA variant stages input tiles with cp.async.bulk.tensor when x is addressable;
+        // the LDG variant needs no tensor map (no driver call on the default path)
         const bool want_tma =
             kernel == SWDFT2D_KERNEL_STREAM_TMA || (kernel == SWDFT2D_KERNEL_AUTO && g_use_tma);
         const K1Info *kt = want_tma ? find_k1(m0, m1, prec, 1) : nullptr;
         if (kt && encode_input_map(kt, x, in_dtype, N0, N1, ld_x, &tmap, &P)) k1 = kt;
-        else encode_input_map(k1, x, in_dtype, N0, N1, ld_x, &tmap, &P);  // fills sample_bytes
-        int occ = 0;
-        if ((rc = k1_occupancy(ds, k1, &occ))) return rc;
+        K1Plan pl;
+        if ((rc = k1_plan(ds, k1, P1, p0_begin, p0_end, &P, &pl))) return rc;
         P.x = x;
         P.in_dtype = in_dtype;
         P.apply_scale = apply ? 1 : 0;
         P.N0 = N0;
         P.N1 = N1;
         P.ldx = ld_x;
-        P.p0_begin = p0_begin;
-        P.p0_end = p0_end;
         P.P1 = P1;
         P.out = out;
         P.scale = scale;
-        P.CB = (P1 + k1->tp1 - 1) / k1->tp1;
-        const int64_t rows = p0_end - p0_begin;
-        const int64_t slots = (int64_t)ds->sms * occ;
-        {
-            std::lock_guard<std::mutex> lk(g_mu);
-            const auto key = std::make_tuple(rows, P.CB, slots, n0);
-            auto it = ds->rch.find(key);
-            if (it == ds->rch.end()) {
-                if (ds->rch.size() > 4096) ds->rch.clear();
-                it = ds->rch.emplace(key, k1_rows_per_tile(rows, P.CB, slots, n0)).first;
-            }
-            P.RCH = it->second;
-        }
-        // One-shot grid of full-height tiles (one CTA per column block, scheduled by the
-        // hardware) for 64-row windows when the column blocks fill >= 3 waves: their 63
-        // warm-up rows make short tiles expensive, and short-lived CTAs write faster than
-        // a persistent grid (profiles/write_probe3_r01.jsonl).  Config 5: 804-810 ->
-        // 825-841 Gcoef/s over three alternations (profiles/k1_oneshot_r01.jsonl).  For
-        // n0 <= 32 the gain was within noise (config 4 +0-1.5 %), so they stay persistent.
-        const bool oneshot = g_k1_oneshot >= 0 ? g_k1_oneshot == 1 : (n0 >= 64 && P.CB >= 3 * slots);
-        if (oneshot && g_k1_oneshot < 0) P.RCH = rows;
-        if (const char *e = std::getenv("SWDFT2D_K1_RCH")) {  // tuning override (rows per tile)
-            const long long v = std::atoll(e);
-            if (v > 0) P.RCH = v < rows ? v : rows;
-        }
-        P.ntiles = P.CB * ((rows + P.RCH - 1) / P.RCH);
-        unsigned long long *ctr = nullptr;
-        // Guided schedule when there are more column blocks than CTA slots (the uniform
-        // chunks then leave a partial last wave: config 4 837 -> 851-857 Gcoef/s, config 3
-        // 724 -> 853, 64x4 / 64x8 / 64x16 on ~8 GB outputs 730-758 -> 817-830) for windows
-        // below 2048 coefficients; the largest (32x64, 64x64: one to two 256-512-thread CTAs
-        // per SM) run 6-9 % slower guided and keep the uniform chunks
-        // (profiles/shape_check_r01d.jsonl).  64-row windows with >= 3 waves of column
-        // blocks take the one-shot grid above instead (config 5: persistent uniform 786,
-        // persistent guided 826-828, one-shot 858-865; profiles/k1_oneshot_r01.jsonl).  Small problems keep the uniform chunks (config 2
-        // would pay the counter's memset and the smaller first tiles: 687 -> 618).
-        // (one-shot grids take the guided chunk sizes only when both are forced: the
-        // hardware then hands the big-first tiles out in blockIdx order, no counter)
-        const bool guided = oneshot ? (g_k1_oneshot == 1 && g_k1_guided == 1)
-                                    : (g_k1_guided >= 0 ? g_k1_guided == 1
-                                                        : (P.CB >= slots && (n0 << m1) < 2048));
-        if (guided) {
-            // guided self-scheduling: each row chunk is about half of the remaining work
-            // spread over the CTAs, so big tiles (little warm-up) go first and small ones
-            // fill the tail
-            int64_t R = rows, off = 0;
-            int nc = 0;
-            const int64_t cmin = n0 > 8 ? n0 : 8;
-            P.chunk[0] = 0;
-            while (R > 0) {
-                int64_t c = (R * P.CB + 2 * slots - 1) / (2 * slots);
-                if (c > (R + 1) / 2) c = (R + 1) / 2;
-                if (c < cmin) c = cmin;
-                if (c > R || nc == K1_MAX_CHUNKS - 1) c = R;
-                off += c;
-                R -= c;
-                P.chunk[++nc] = off;
-            }
-            P.nchunks = nc;
-            P.ntiles = P.CB * nc;
-            if (!oneshot &&
-                (cudaMallocAsync((void **)&ctr, sizeof(unsigned long long), st) != cudaSuccess ||
-                 cudaMemsetAsync(ctr, 0, sizeof(unsigned long long), st) != cudaSuccess))
-                return fail(SWDFT2D_E_NOMEM, "K1 tile counter: %s", cudaGetErrorString(cudaGetLastError()));
-            P.counter = ctr;  // nullptr for a one-shot grid: one tile per CTA
-        }
-        {
-            const void *tw64 = nullptr, *tw32 = nullptr;
-            if ((rc = k0_tables(ds, &tw64, &tw32))) return rc;
-            P.tw = static_cast<const double2 *>(tw64);
-        }
-        const int64_t grid = (oneshot || P.ntiles < slots) ? P.ntiles : slots;
-        k1->launch(P, tmap, (int)grid, st);
-        if (ctr) cudaFreeAsync(ctr, st);
+        P.tw = static_cast<const double2 *>(tw64);
+        P.counter = nullptr;  // one-shot grids take one tile per CTA: no counter
+        if (pl.guided && !pl.oneshot && (rc = k1_counter(ds, st, &P.counter))) return rc;
+        k1->launch(P, tmap, (int)pl.grid, st);
     } else {
-        if (m0 > SWDFT2D_K0_MAX_M || m1 > SWDFT2D_K0_MAX_M)
-            return fail(SWDFT2D_E_UNSUPPORTED, "window 2^%d x 2^%d exceeds the CUDA paths (max 2^%d)",
-                        m0, m1, SWDFT2D_K0_MAX_M);
-        const void *tw64 = nullptr, *tw32 = nullptr;
-        if ((rc = k0_tables(ds, &tw64, &tw32))) return rc;
         K0Params P;
         std::memset(&P, 0, sizeof P);
         P.x = x;
@@ -616,7 +774,7 @@ int swdft2d_forward(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t
         P.P1 = P1;
         P.out = out;
         P.scale = scale;
-        P.tw = prec == SWDFT2D_PREC_FP64 ? tw64 : tw32;
+        P.tw = tw;
         P.tw_n = K0_TW_N;
         if (launch_k0(P, prec, st))
             return fail(SWDFT2D_E_UNSUPPORTED, "K0 grid too large for %lld x %lld outputs",
@@ -850,6 +1008,10 @@ int swdft2d_shutdown(void) {
             cudaSetDevice(kv.first);
             cudaFree(kv.second.k0_tw64);
             cudaFree(kv.second.k0_tw32);
+        }
+        if (!kv.second.ctr_blocks.empty()) {
+            cudaSetDevice(kv.first);
+            for (unsigned long long *b : kv.second.ctr_blocks) cudaFree(b);
         }
     }
     g_dev.clear();

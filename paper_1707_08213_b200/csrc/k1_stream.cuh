@@ -361,7 +361,15 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
             __syncthreads();
         }
         if (P.counter) {  // guided: the next tile from the shared counter (after the first wave)
-            if (tid == 0) s_next = (int64_t)atomicAdd(P.counter, 1ull) + gridDim.x;
+            // A launch makes exactly ntiles fetches (ntiles - grid real tiles, then one
+            // terminating fetch per CTA), so the fetch that returns ntiles - 1 is the last
+            // one: it zeroes the counter for the next launch on this stream (the counter is
+            // a per-(device, stream) slot allocated once, abi.cu k1_counter).
+            if (tid == 0) {
+                const unsigned long long v = atomicAdd(P.counter, 1ull);
+                if (v == (unsigned long long)(P.ntiles - 1)) atomicExch(P.counter, 0ull);
+                s_next = (int64_t)v + gridDim.x;
+            }
             __syncthreads();
             tile = s_next;
         } else {

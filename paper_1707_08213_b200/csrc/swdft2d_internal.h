@@ -9,8 +9,10 @@
 namespace swdft2d {
 
 constexpr int K2_TW_N = 64;   // make_twiddles(64): K2 (stream push) windows up to 64
-constexpr int K1_MAX_CHUNKS = 48;  // guided K1 schedule: row chunks per launch    // K1 twiddle table: make_twiddles(64), read at stride 64/n
-constexpr int K0_TW_N = 1024;  // K0 twiddle table: make_twiddles(1024), in device memory
+constexpr int K1_MAX_CHUNKS = 48;  // guided K1 schedule: row chunks per launch
+// device twiddle table make_twiddles(1024) (fp64 and fp32 copies), allocated once per
+// device; every kernel reads it at stride 1024/n (bitwise make_twiddles(n), App. A #4)
+constexpr int K0_TW_N = 1024;
 
 struct K0Params {
     const void *x;
@@ -34,7 +36,8 @@ struct K1Params {
     int64_t ntiles;  // CB * number of row chunks
     // guided schedule (nchunks > 0): row chunk c covers window rows
     // [p0_begin + chunk[c], p0_begin + chunk[c + 1]); tiles past the first wave are
-    // handed out by atomicAdd on *counter (zeroed before the launch)
+    // handed out by atomicAdd on *counter (zero at launch; the launch's last fetch zeroes
+    // it again, so one per-(device, stream) counter serves every launch on that stream)
     int nchunks;
     unsigned long long *counter;
     int64_t chunk[K1_MAX_CHUNKS + 1];

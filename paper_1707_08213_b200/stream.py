@@ -67,6 +67,8 @@ class SlidingRowStream2D:
                                                             ctypes.byref(nbytes)))
             self._state = torch.zeros(max(1, nbytes.value), dtype=torch.uint8, device=self.device)
         self._state_rows = 0  # rows the state has absorbed (== rows_pushed unless push_rows ran)
+        self._pins = {}  # host-row upload ring per dtype (_upload)
+        self._pin_next = 0
         self._ring_ptr = self._ring.data_ptr()
         self._dev_index = self.device.index if self.device.index is not None else \
             torch.cuda.current_device()
@@ -147,8 +149,10 @@ class SlidingRowStream2D:
         r = _to_tensor(row)
         if tuple(r.shape) != (self.N1,):
             raise core.ShapeError(f"row shape {tuple(r.shape)} != ({self.N1},)")
-        if r.device != self.device:
-            r = r.to(self.device, non_blocking=(not r.is_cuda) and r.is_pinned())
+        if not r.is_cuda:
+            r = self._upload(r)
+        elif r.device != self.device:
+            r = r.to(self.device)
         if r.stride(0) != 1:
             r = r.contiguous()
         p0 = self.rows_pushed
@@ -169,6 +173,28 @@ class SlidingRowStream2D:
         self.rows_pushed += 1
         self._state_rows = self.rows_pushed
         return slab
+
+    _UPLOAD_SLOTS = 4
+
+    def _upload(self, r):
+        """Host row -> device through a library-owned pinned ring: the caller's buffer is
+        read synchronously here (so it may be refilled as soon as push_row returns) and the
+        H2D copy of the pinned slot stays asynchronous; a slot is refilled only after its
+        previous copy has completed (its event)."""
+        slots = self._pins.get(r.dtype)
+        if slots is None:
+            slots = self._pins[r.dtype] = [
+                (torch.empty(self.N1, dtype=r.dtype, pin_memory=True),
+                 torch.empty(self.N1, dtype=r.dtype, device=self.device), torch.cuda.Event())
+                for _ in range(self._UPLOAD_SLOTS)]
+        host, dev, ev = slots[self._pin_next % self._UPLOAD_SLOTS]
+        self._pin_next += 1
+        ev.synchronize()  # no-op until the slot was used (an unrecorded event is complete)
+        host.copy_(r.reshape(-1))
+        with torch.cuda.device(self.device):
+            dev.copy_(host, non_blocking=True)
+            ev.record()
+        return dev
 
     def _push(self, r, state, p0, slab) -> int:
         stream = _lib.raw_stream(self._dev_index)

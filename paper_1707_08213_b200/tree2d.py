@@ -116,15 +116,41 @@ def forward_into(xt: torch.Tensor, m0: int, m1: int, out: torch.Tensor, *, prec:
         raise ValueError("x and out must be on the same device")
     dev = xt.device.index
     sp = stream.cuda_stream if stream is not None else _lib.raw_stream(dev)
+    kcode = _lib.KERNELS[kernel]
+    # the large-window path's workspace comes from torch's allocator (PyTorch owns every
+    # device buffer; the library allocates nothing per call when given one)
+    wkey = (N0, N1, m0, m1, prec, p0_begin, p0_end, kcode)
+    wbytes = _WS_BYTES.get(wkey)
+    if wbytes is None:
+        wbytes = _lib.workspace_bytes(N0, N1, m0, m1, prec, p0_begin, p0_end, kcode)
+        if len(_WS_BYTES) > 4096:
+            _WS_BYTES.clear()
+        _WS_BYTES[wkey] = wbytes
+    ws = None
+    if wbytes:
+        with torch.cuda.stream(stream) if stream is not None else _nullctx():
+            ws = torch.empty(wbytes, dtype=torch.uint8, device=xt.device)
     args = (xt.data_ptr(), _IN_CODES[xt.dtype], N0, N1, xt.stride(0), m0, m1, prec, float(scale),
-            p0_begin, p0_end, out.data_ptr(), _lib.KERNELS[kernel], sp)
+            p0_begin, p0_end, out.data_ptr(), ws.data_ptr() if ws is not None else None, wbytes,
+            kcode, sp)
     if torch.cuda.current_device() == dev:
-        rc = lib.swdft2d_forward(*args)
+        rc = lib.swdft2d_forward_ws(*args)
     else:
         with torch.cuda.device(dev):
-            rc = lib.swdft2d_forward(*args)
+            rc = lib.swdft2d_forward_ws(*args)
     _lib.check(rc)
     return out
+
+
+_WS_BYTES: dict = {}
+
+
+class _nullctx:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
 
 
 def _forward_to_host(xt, m0, m1, host, prec, scale, kernel, strip_bytes, slots=4, copiers=2):
@@ -206,12 +232,15 @@ def tree_swdft_2d(x, spec, loop_order: str = "levels-outer", counter=None, budge
     if device is None:
         device = xt.device if xt.is_cuda else torch.device("cuda", torch.cuda.current_device())
     device = torch.device(device)
+    host_mode = to_host or host_out is not None
     if not xt.is_cuda or xt.device != device:
-        xt = xt.to(device, non_blocking=xt.is_pinned() if not xt.is_cuda else False)
+        # asynchronous only in host-output mode, which synchronizes before returning; a
+        # call returning a device tensor must not leave a DMA reading the caller's buffer
+        xt = xt.to(device, non_blocking=host_mode and not xt.is_cuda and xt.is_pinned())
     n0, n1 = 1 << m0, 1 << m1
     P0, P1 = shape[0] - n0 + 1, shape[1] - n1 + 1
     scale = core.normalization_factor(spec)
-    if to_host or host_out is not None:
+    if host_mode:
         # host (numpy) output, as the reference returns: strips computed in a small
         # device ring and streamed to pinned host memory while the next strips compute
         want = (P0, P1, n0, n1)

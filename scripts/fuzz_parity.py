@@ -41,6 +41,8 @@ def main():
     ap.add_argument("--cases", type=int, default=400)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--max-coefs", type=float, default=6e6)
+    ap.add_argument("--k1-only", action="store_true",
+                    help="windows 2..64 x 1..64 only (K1), e.g. under SWDFT2D_K1_* overrides")
     a = ap.parse_args()
     oracle.build()
     dev = torch.device("cuda", 0)
@@ -53,8 +55,12 @@ def main():
     for case in range(a.cases):
         u = rng.random()
         big, tall = u < 0.15, 0.15 <= u < 0.25  # tall: K1's 128/256-row windows
+        if a.k1_only:
+            big = tall = False
         m0 = int(rng.integers(7, 10)) if tall else int(rng.integers(0, 11 if big else 7))
         m1 = int(rng.integers(0, 6)) if tall else int(rng.integers(0, 11 if big else 7))
+        if a.k1_only and m0 == 0:
+            m0 = int(rng.integers(1, 7))
         n0, n1 = 1 << m0, 1 << m1
         # shape: window + extra, bounded output size
         for _ in range(50):
@@ -100,7 +106,9 @@ def main():
             print(json.dumps({"case": case, "m": [m0, m1], "N": [N0, N1], "dtype": np.dtype(dt).name,
                               "pad": pad, "rows": [p0a, p0b], "norm": norm, "kernel": kind,
                               "max_abs_diff": float(d.max()), "fp32_rel": rel32}), flush=True)
-    print(json.dumps({"cases": a.cases, "fails": fails, "by_kernel": kinds,
+    done = sum(kinds.values())
+    print(json.dumps({"cases": done, "requested": a.cases, "fails": fails,
+                      "env": {k: v for k, v in os.environ.items() if k.startswith("SWDFT2D_")}, "by_kernel": kinds,
                       "fp32_worst_window_rel_err": worst32,
                       "seconds": round(time.time() - t0, 1)}), flush=True)
     return 1 if fails else 0

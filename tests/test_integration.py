@@ -1,0 +1,134 @@
+"""The reference's own entry point served by the B200 library (integration/swdft_b200.py).
+
+The UNMODIFIED reference package is staged into the git-ignored baseline/_ref/ by
+scripts/stage_reference.sh (run by __graft_entry__.build() where /root/reference
+exists; the copy travels to the GPU box with the snapshot).  These tests import
+``swdft`` from there, enable the backend, and check the drop-in contract against the
+reference's own types, exceptions, counter and golden outputs.
+"""
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, sha
+from golden_inputs import kat6_input
+
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+INTEG_DIR = os.path.join(ROOT, "integration")
+
+
+@pytest.fixture(scope="module")
+def swdft():
+    if not os.path.isfile(os.path.join(REF_DIR, "swdft", "tree2d.py")):
+        pytest.skip("reference package not staged (scripts/stage_reference.sh)")
+    for d in (REF_DIR, INTEG_DIR):
+        if d not in sys.path:
+            sys.path.insert(0, d)
+    import swdft.bench
+    import swdft.core
+    import swdft.tree2d
+    import swdft_b200
+
+    orig = swdft.tree2d.tree_swdft_2d
+    swdft_b200.enable()
+    assert swdft.tree2d.tree_swdft_2d is not orig and swdft_b200.enabled()
+    yield swdft
+    swdft_b200.disable()
+    assert swdft.tree2d.tree_swdft_2d is orig
+
+
+def test_reference_exceptions_through_backend(swdft):
+    """Validation runs before any device work, with the reference's classes and messages."""
+    core, tree2d = swdft.core, swdft.tree2d
+    spec = core.WindowSpec.from_sizes((4, 4))
+    with pytest.raises(core.ShapeError):
+        tree2d.tree_swdft_2d(np.zeros((4, 4, 4)), spec)
+    with pytest.raises(core.WindowTooLargeError):
+        tree2d.tree_swdft_2d(np.zeros((3, 8)), spec)
+    with pytest.raises(ValueError, match="loop_order"):
+        tree2d.tree_swdft_2d(np.zeros((8, 8)), spec, loop_order="rows-first")
+    with pytest.raises(core.BudgetError) as e:
+        tree2d.tree_swdft_2d(np.zeros((64, 64)), spec, budget=1000)
+    # the same numbers and text the reference's own implementation raises
+    import swdft_b200
+
+    with pytest.raises(core.BudgetError) as e_ref:
+        swdft_b200._STATE["orig"](np.zeros((64, 64)), spec, budget=1000)
+    assert str(e.value) == str(e_ref.value)
+    assert e.value.required_bytes == e_ref.value.required_bytes
+    with pytest.raises(core.InvalidWindowError):
+        core.WindowSpec.from_sizes((3, 4))
+
+
+@pytest.mark.gpu
+def test_reference_entry_point_bitwise(swdft, golden, cuda):
+    core, tree2d = swdft.core, swdft.tree2d
+    meta, arr = golden
+    x = np.array(meta["kat"]["kat1"]["x"])
+    r = tree2d.tree_swdft_2d(x, core.WindowSpec.from_sizes((2, 2)))
+    assert isinstance(r, core.CoefficientArray)
+    assert isinstance(r.values, np.ndarray) and r.values.dtype == np.complex128
+    assert np.array_equal(r.values.view(np.uint64), arr["kat1_out"].view(np.uint64))
+    r = tree2d.tree_swdft_2d(np.ones((8, 8)), core.WindowSpec.from_sizes((4, 4)))
+    assert np.array_equal(r.values.view(np.uint64), arr["kat2_out"].view(np.uint64))
+    k6, nx = kat6_input()
+    r = tree2d.tree_swdft_2d(k6, core.WindowSpec.from_sizes((2, 4)))
+    assert np.array_equal(r.values.view(np.uint64), arr["kat6_out"].view(np.uint64))
+    for mode in ("unitary", "paper-2d"):
+        spec = core.WindowSpec((2, 1), mode)
+        r = tree2d.tree_swdft_2d(nx, spec)
+        assert r.normalization == mode
+        assert np.array_equal(r.values.view(np.uint64), arr[f"norm_{mode}_out"].view(np.uint64))
+        with pytest.raises(core.StateError):  # the record behaves like normalize()'s output
+            core.normalize(r, mode)
+    from paper_1707_08213_b200.workloads import CONFIGS
+
+    cfg = CONFIGS["c1"]
+    r = tree2d.tree_swdft_2d(cfg.generate(), core.WindowSpec((cfg.m0, cfg.m1)))
+    assert sha(r.values) == meta["configs"]["c1"]["full_sha"]
+
+
+@pytest.mark.gpu
+def test_reference_entry_point_matches_reference_run(swdft, cuda):
+    """Same output bits and the same OpCounter state as the reference's own numpy code
+    on the same inputs (both loop orders, a normalization mode, odd shapes)."""
+    import swdft_b200
+
+    core, tree2d, bench = swdft.core, swdft.tree2d, swdft.bench
+    orig = swdft_b200._STATE["orig"]
+    rng = np.random.default_rng(8)
+    for shape, sizes, mode in [((37, 29), (4, 8), "none"), ((20, 33), (8, 2), "unitary"),
+                               ((16, 16), (16, 1), "paper-2d"), ((9, 40), (1, 32), "none")]:
+        x = rng.standard_normal(shape) + 1j * rng.standard_normal(shape)
+        spec = core.WindowSpec(tuple(int(s).bit_length() - 1 for s in sizes), mode)
+        for order in tree2d.LOOP_ORDERS:
+            c_ref, c_b200 = bench.OpCounter(shape), bench.OpCounter(shape)
+            ref = orig(x, spec, loop_order=order, counter=c_ref)
+            got = tree2d.tree_swdft_2d(x, spec, loop_order=order, counter=c_b200, threads=4)
+            assert got.normalization == ref.normalization == mode
+            assert got.source_shape == ref.source_shape
+            assert np.array_equal(got.values.view(np.uint64), ref.values.view(np.uint64))
+            assert c_b200.total == c_ref.total
+            assert np.array_equal(c_b200.position_ops, c_ref.position_ops)
+
+
+@pytest.mark.gpu
+def test_reference_entry_point_device_values(swdft, cuda):
+    import torch
+
+    import swdft_b200
+
+    core, tree2d = swdft.core, swdft.tree2d
+    x = np.random.default_rng(2).standard_normal((70, 90))
+    spec = core.WindowSpec.from_sizes((16, 16))
+    host = tree2d.tree_swdft_2d(x, spec)
+    swdft_b200.enable(values="device")
+    try:
+        dev = tree2d.tree_swdft_2d(x, spec)
+    finally:
+        swdft_b200.enable(values="numpy")
+    assert isinstance(dev, core.CoefficientArray) and isinstance(dev.values, torch.Tensor)
+    assert dev.values.is_cuda and dev.values.dtype == torch.complex128
+    assert np.array_equal(dev.values.cpu().numpy().view(np.uint64), host.values.view(np.uint64))

@@ -132,6 +132,32 @@ def test_row_stream_equals_batch(cuda, oracle_lib, shape, m, kernel):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("pinned", [True, False])
+def test_row_stream_reused_host_buffer(cuda, oracle_lib, pinned):
+    """The usual streaming pattern: ONE host row buffer refilled before every push, no
+    synchronisation by the caller.  push_row reads the caller's buffer before returning
+    (an asynchronous H2D straight from it read the next row's data)."""
+    import torch
+
+    from paper_1707_08213_b200.stream import SlidingRowStream2D
+
+    shape, m = (300, 2000), (4, 4)
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal(shape)
+    ref = oracle_lib.tree2d(x, *m)
+    st = SlidingRowStream2D(WindowSpec(m), shape[1])
+    buf = torch.empty(shape[1], dtype=torch.float64, pin_memory=pinned)
+    slabs = []
+    for p0 in range(shape[0]):
+        buf.copy_(torch.from_numpy(x[p0]))
+        s = st.push_row(buf)
+        if s is not None:
+            slabs.append(s)
+    got = torch.stack(slabs).cpu().numpy()
+    assert np.array_equal(got.view(np.uint64), ref.view(np.uint64))
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("shape,m", [((40, 21), (2, 2)), ((70, 130), (6, 6)), ((9, 12), (3, 1))])
 def test_row_stream_blocks_equal_batch(cuda, oracle_lib, shape, m):
     """push_rows(block) == the same rows pushed one by one == the batch rows."""
