@@ -19,12 +19,15 @@ Default workload: config 4 (4096x4096 f32 image-like array, 16x16 windows,
   cpu_baseline  the C restatement of the reference (oracle/, all host threads)
              on the first window rows of the same config (rank 0, N=1 only)
 
-N > 1 (torchrun, one process per GPU, NCCL), --scaling weak (default): every rank
-transforms its own config-sized workload (generated locally) with no data-path
-collective; value = N x coefficients / (max over ranks of the step time).
---scaling strong: ONE workload partitioned into window-row strips; rank 0 holds
-the input in HBM and each step = pipelined scatter of input row strips with
-halos (NCCL send/recv from rank 0) + every rank's strip of the transform.
+N > 1 (torchrun, one process per GPU, NCCL), --scaling strong (default): ONE
+workload partitioned into window-row strips, the north-star deployment; rank 0
+holds the input in HBM and each step = pipelined scatter of input row strips with
+their halos (NCCL send/recv from rank 0, piece-major: every rank's first chunk
+first) + every rank's strip of the transform; value = coefficients / (max over
+ranks of the step time).  The line's "strong" object adds the scatter alone, the
+compute alone and an in-run N=1 time of the same workload on rank 0, with
+E(N) = t(1) / (N t(N)).  --scaling weak: every rank transforms its own
+config-sized workload (generated locally) with no data-path collective.
 
 --impl reference: times the CPU reference path (the oracle's C restatement of
 the reference's levels-outer tree, all host threads) on a bounded sample of the
@@ -83,13 +86,15 @@ def measured_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(config: str):
-    """dram bytes per launch of the dominant kernel from the committed ncu capture."""
+def ncu_traffic(config: str, precision: str):
+    """dram bytes (read + write) per full launch of the dominant kernel, from the committed
+    ncu capture of this config AND precision (profiles/ncu_summary.json "<config>/<prec>");
+    None when no such full-launch capture exists."""
     p = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        e = d.get(config)
+        e = d.get(f"{config}/{precision}")
         return None if e is None else float(e["dram_bytes_per_launch"])
     except (OSError, KeyError, ValueError):
         return None
@@ -169,6 +174,47 @@ def cpu_reference_rate(cfg, rows: int, reps: int, threads: int):
     return coefs / statistics.median(times), times, coefs
 
 
+def numpy_reference_rate(cfg, rows: int, threads: int):
+    """Coefficients/s of the UNMODIFIED reference (swdft.tree2d.tree_swdft_2d, numpy,
+    staged into baseline/_ref by scripts/stage_reference.sh) on window rows [0, rows) of
+    the config, `threads` as its own thread-pool argument.  None if it is not staged."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isfile(os.path.join(ref, "swdft", "tree2d.py")):
+        return None
+    if ref not in sys.path:
+        sys.path.insert(0, ref)
+    from swdft import core as rcore
+    from swdft import tree2d as rtree
+
+    x = cfg.generate(rows=rows + cfg.n0 - 1)
+    spec = rcore.WindowSpec((cfg.m0, cfg.m1))
+    t0 = time.perf_counter()
+    r = rtree.tree_swdft_2d(x, spec, threads=threads, budget=1 << 42)
+    t = time.perf_counter() - t0
+    coefs = r.values.size
+    del r
+    return {"value": coefs / t, "unit": UNIT, "cores": threads, "seconds": t,
+            "sample": f"window rows [0,{rows}) of {cfg.name} ({coefs} coefficients)"}
+
+
+def cpu_context(cfg, rows_port: int, rows_numpy: int):
+    """BASELINE.md's CPU plan as context next to cpu_baseline: the C port at T=1 and the
+    reference's own numpy code at T=1 and T=all cores (smaller sample: it is ~15x slower)."""
+    ctx = {"cpu_model": cpu_model(), "host_cores": host_cores()}
+    rate, t, coefs = cpu_reference_rate(cfg, rows_port, 1, 1)
+    ctx["port_1_thread"] = {"value": rate, "unit": UNIT, "cores": 1, "seconds": t[0],
+                            "sample": f"window rows [0,{rows_port}) of {cfg.name} ({coefs} "
+                                      "coefficients), oracle/swdft2d_oracle.c"}
+    for name, th in (("numpy_reference_1_thread", 1), ("numpy_reference_all_cores", host_cores())):
+        try:
+            r = numpy_reference_rate(cfg, rows_numpy, th)
+        except Exception as e:  # noqa: BLE001 - context only; say why it is missing
+            r = {"unavailable": f"{type(e).__name__}: {e}"}
+        ctx[name] = r if r is not None else {
+            "unavailable": "reference not staged (scripts/stage_reference.sh)"}
+    return ctx
+
+
 def run_reference(args, cfg, rank):
     if rank != 0:
         return
@@ -194,7 +240,9 @@ def run_reference(args, cfg, rank):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json recipe)",
         "config": {"workload": cfg.name, "desc": cfg.desc, "sample_window_rows": rows},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                         "sample": sample},
+                         "sample": sample,
+                         "numpy_reference_all_cores": numpy_reference_rate(
+                             cfg, min(rows, 32), threads)},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -225,7 +273,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     # own share of window rows of an N-times taller array, generated locally): no
     # data-path collective, per-GPU work fixed.  "strong" — the north-star partition of
     # ONE workload: window-row strips scattered from rank 0 over NCCL (pipelined).
-    strips = world > 1 and args.scaling == "strong"
+    strips = (world > 1 or args.strips) and args.scaling == "strong"
     x_np = cfg.generate() if (rank == 0 or not strips) else None
     xdt = {"float32": torch.float32, "float64": torch.float64, "complex64": torch.complex64,
            "complex128": torch.complex128}[cfg.dtype]
@@ -328,7 +376,8 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "scatter_pieces": pieces},
         "hbm_write_gbs": units * out_bpc / step_s / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": ncu_traffic(cfg.name),
+                     "frac": achieved / peak,
+                     "traffic": ncu_traffic(cfg.name, "fp32" if prec == _lib.PREC_FP32 else "fp64"),
                      "peak_source": peak_src,
                      # BASELINE.md's target is quoted against the 8.0 TB/s nominal HBM peak
                      "nominal_peak": 8000.0, "frac_nominal": achieved / 8000.0,
@@ -339,18 +388,20 @@ def run_ours(args, cfg, rank, world, local_rank):
         "gpu_launches": args.steps * pieces,
     }
 
+    if strips and not args.no_strong_detail:
+        line["strong"] = strong_detail(args, cfg, rank, world, dev, stream, x_full, recv, out,
+                                       prec, pieces, step_s, graph_free=True)
+
     # e2e through the public API from pinned host memory
     if not args.no_e2e:
         if not strips:
             line["e2e"] = e2e_host(args, cfg, x_np, dev, spec, odt, out, world)
         else:
-            del out
+            out = None
             torch.cuda.empty_cache()
             line["e2e"] = e2e_sharded(args, cfg, x_np, dev, spec, xdt, prec, rank, world)
     if world == 1 and not args.no_others:
-        if graph is not None:
-            del graph
-        del out
+        graph = out = None
         torch.cuda.empty_cache()
         line["other_configs"] = other_configs(args, cfg, dev, flush, stream)
     if world == 1 and not args.no_cpu:
@@ -360,8 +411,75 @@ def run_ours(args, cfg, rank, world, local_rank):
             "sample": f"window rows [0,{args.ref_rows}) of {cfg.name} ({coefs} coefficients), "
                       f"median of 3, C restatement of the reference levels-outer tree "
                       f"(oracle/swdft2d_oracle.c, complex128) on {cpu_model()}"}
+        if not args.no_cpu_context:
+            line["cpu_baseline"]["context"] = cpu_context(cfg, args.ref_rows,
+                                                          min(args.ref_rows, 32))
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def strong_detail(args, cfg, rank, world, dev, stream, x_full, recv, out, prec, pieces, step_s,
+                  graph_free=True):
+    """Strong-scaling breakdown (max over ranks, device-timed, L2 flushed): the pipelined
+    scatter alone (compute replaced by nothing), each rank's strip transform alone (input
+    already resident), and t(1) = the whole workload on rank 0 alone in the same run, so
+    E(N) = t(1) / (N t(N)) needs no other run."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1707_08213_b200.partition import pipelined_strip_forward, strip_plan
+    from paper_1707_08213_b200.tree2d import _OUT_DTYPES, forward_into
+
+    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
+    a, b, rb, re = strip_plan(cfg.P0, cfg.m0, world)[rank]
+    xdt = x_full.dtype if x_full is not None else recv.dtype
+    local = x_full[rb:re] if x_full is not None else recv
+
+    def timed(fn, reps):
+        ts = []
+        for _ in range(reps):
+            dist.barrier()
+            torch.cuda.synchronize()
+            flush_l2(flush)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ts.append(e0.elapsed_time(e1) / 1e3)
+        t = torch.tensor([statistics.median(ts)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def scatter_only():
+        pipelined_strip_forward(x_full if rank == 0 else None, (cfg.N0, cfg.N1), cfg.m0, xdt,
+                                dev, lambda *_: None, recv=recv, pieces=pieces)
+
+    def compute_only():
+        if b > a:
+            forward_into(local, cfg.m0, cfg.m1, out, prec=prec, p0_begin=0, p0_end=b - a,
+                         stream=stream)
+
+    reps = max(3, min(args.steps, 5))
+    t_scatter = timed(scatter_only, reps)
+    t_compute = timed(compute_only, reps)
+    # t(1): rank 0 transforms the whole workload alone (the other ranks idle)
+    full = None
+    if rank == 0:
+        full = torch.empty((cfg.P0, cfg.P1, cfg.n0, cfg.n1), dtype=_OUT_DTYPES[prec], device=dev)
+        forward_into(x_full, cfg.m0, cfg.m1, full, prec=prec, stream=stream)
+
+    def one_gpu():
+        if rank == 0:
+            forward_into(x_full, cfg.m0, cfg.m1, full, prec=prec, stream=stream)
+
+    t1 = timed(one_gpu, reps)
+    del full
+    torch.cuda.empty_cache()
+    return {"t1_ms": t1 * 1e3, "tN_ms": step_s * 1e3, "efficiency_in_run": t1 / (world * step_s),
+            "scatter_only_ms": t_scatter * 1e3, "compute_only_ms": t_compute * 1e3,
+            "scatter_pieces": pieces,
+            "note": "max over ranks, median of %d; t1 = whole workload on rank 0 alone, same run" % reps}
 
 
 def other_configs(args, main_cfg, dev, flush, stream):
@@ -375,10 +493,13 @@ def other_configs(args, main_cfg, dev, flush, stream):
 
     peak, _ = measured_peak()
     res = {}
-    for name, c in CONFIGS.items():
-        if name == main_cfg.name:
-            continue
-        prec = _precision_code(c.precision, None)
+    # every other config at its BASELINE precision, plus the headline config in fp64 — the
+    # reference's own precision (complex128, bitwise equal to the reference)
+    runs = [(name, c, c.precision) for name, c in CONFIGS.items() if name != main_cfg.name]
+    if main_cfg.precision != "fp64":
+        runs.append((f"{main_cfg.name}_fp64", main_cfg, "fp64"))
+    for name, c, pname in runs:
+        prec = _precision_code(pname, None)
         x = torch.from_numpy(c.generate()).to(dev)
         out = torch.empty((c.P0, c.P1, c.n0, c.n1), dtype=_OUT_DTYPES[prec], device=dev)
         for _ in range(3):
@@ -401,11 +522,18 @@ def other_configs(args, main_cfg, dev, flush, stream):
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1) / 1e3)
         t = statistics.median(ts)
-        alg = c.algorithmic_bytes()
+        alg = c.algorithmic_bytes(precision=pname)
+        traffic = ncu_traffic(c.name, pname)
         res[name] = {"desc": c.desc, "dtype": "f32" if prec == _lib.PREC_FP32 else "f64",
                      "value": c.coefficients / t, "unit": UNIT, "kernel_ms": t * 1e3,
-                     "hbm_write_gbs": c.coefficients * c.out_bytes_per_coef / t / 1e9,
-                     "roofline_frac": alg / t / 1e9 / peak}
+                     "hbm_write_gbs": c.coefficients * (16 if pname == "fp64" else 8) / t / 1e9,
+                     "roofline": {"bound": "hbm", "achieved": alg / t / 1e9, "peak": peak,
+                                  "unit": "GB/s", "frac": alg / t / 1e9 / peak,
+                                  "frac_nominal": alg / t / 1e9 / 8000.0, "traffic": traffic,
+                                  "traffic_over_alg": None if traffic is None else traffic / alg},
+                     "roofline_frac": alg / t / 1e9 / peak,
+                     "kernel": dict(_lib.stream_kernel_info(c.m0, c.m1, prec),
+                                    schedule=_lib.k1_schedule(c.N0, c.N1, c.m0, c.m1, prec)["mode"])}
         del g, x, out
         torch.cuda.empty_cache()
     return res
@@ -551,11 +679,19 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cpu-context", action="store_true",
+                    help="skip the T=1 port and numpy-reference timings next to cpu_baseline")
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-others", action="store_true", help="skip the other-configs summary")
-    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
-                    help="N>1: weak = every rank its own workload, no collective (default); "
-                         "strong = one workload in strips scattered from rank 0 over NCCL")
+    ap.add_argument("--strips", action="store_true",
+                    help="run the strip path (pipelined scatter + per-strip K1) even at N=1 "
+                         "(under torchrun; exercises the N>1 code on one GPU)")
+    ap.add_argument("--no-strong-detail", action="store_true",
+                    help="N>1 strong: skip the scatter-only / compute-only / t(1) breakdown")
+    ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],
+                    help="N>1: strong = ONE workload in window-row strips scattered from rank 0 "
+                         "over NCCL, the north-star partition (default); weak = every rank its "
+                         "own workload, no data-path collective")
     ap.add_argument("--precision", default=None, choices=[None, "fp32", "fp64"],
                     help="override the config's precision (fp64 = DAG-exact complex128)")
     args = ap.parse_args()
@@ -572,7 +708,10 @@ def main():
     if args.impl == "reference":
         run_reference(args, cfg, rank)
         return
-    if world > 1:
+    dist_on = world > 1 or (args.strips and "RANK" in os.environ)
+    if args.strips and not dist_on:
+        ap.error("--strips needs a torchrun launch")
+    if dist_on:
         import torch
         import torch.distributed as dist
 
@@ -581,7 +720,7 @@ def main():
     try:
         run_ours(args, cfg, rank, world, local_rank)
     finally:
-        if world > 1:
+        if dist_on:
             import torch.distributed as dist
 
             dist.destroy_process_group()

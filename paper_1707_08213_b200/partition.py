@@ -32,6 +32,18 @@ def strip_plan(P0: int, m0: int, world: int):
     return [_lib.strip_range(P0, m0, g, world) for g in range(world)]
 
 
+def block_plan(P0: int, P1: int, m0: int, m1: int, gr: int, gc: int):
+    """2-D partition over gr x gc ranks (rank g = i * gc + j): window rows
+    [floor(P0 i/gr), floor(P0 (i+1)/gr)) x window columns [floor(P1 j/gc),
+    floor(P1 (j+1)/gc)), i.e. the strip rule on each axis, with the n0 - 1 halo input
+    rows and n1 - 1 halo input columns.  Row strips are (G, 1).  Column blocks are
+    bitwise exact like row strips.
+    [(p0_begin, p0_end, p1_begin, p1_end, row_begin, row_end, col_begin, col_end)]."""
+    rows = strip_plan(P0, m0, gr)
+    cols = strip_plan(P1, m1, gc)
+    return [(r[0], r[1], c[0], c[1], r[2], r[3], c[2], c[3]) for r in rows for c in cols]
+
+
 def strip_plan_py(P0: int, m0: int, world: int):
     """Pure-Python statement of the same rule (used to cross-check the C ABI)."""
     n0 = 1 << m0
@@ -44,7 +56,8 @@ def strip_plan_py(P0: int, m0: int, world: int):
 
 @dataclass
 class ShardedCoefficients:
-    """This rank's window rows of the [P0, P1, n0, n1] output (device resident)."""
+    """This rank's block of the [P0, P1, n0, n1] output (device resident): window rows
+    [p0_begin, p0_end) x window columns [p1_begin, p1_end) (all columns for row strips)."""
 
     values: torch.Tensor
     p0_begin: int
@@ -52,6 +65,8 @@ class ShardedCoefficients:
     source_shape: tuple
     window: object
     normalization: str = "none"
+    p1_begin: int = 0
+    p1_end: int | None = None
 
 
 def scatter_strips(x, shape, m0: int, dtype, device, group=None, src: int = 0, recv=None):
@@ -126,53 +141,88 @@ def choose_pieces(shape, m0: int, m1: int, in_bytes: int, out_bytes: int, world:
     return 2 if send_all - send_first > (n0 - 1) * row_t + 5e-6 else 1
 
 
-def pipelined_strip_forward(x, shape, m0: int, dtype, device, compute, group=None, src: int = 0,
-                            recv=None, pieces: int = 2, first_fraction: float = 0.125):
-    """Scatter + compute with overlap: every rank's strip travels as ``pieces``
-    consecutive row chunks (separate point-to-point messages, in order), and
-    ``compute(local_rows, w_begin, w_end)`` runs for window rows [w_begin, w_end)
-    (strip-relative) as soon as the input rows they need, [w_begin, w_end + n0 - 1),
-    have arrived — so rank g starts after its first (short) chunk instead of after
-    its whole strip.  The source rank computes its own strip at once.
-    Returns (local_rows_tensor, (p0_begin, p0_end, row_begin, row_end)).
-    """
+def pipelined_block_forward(x, shape, m0: int, m1: int, split, dtype, device, compute,
+                            group=None, src: int = 0, recv=None, pieces: int = 2,
+                            first_fraction: float = 0.125):
+    """Scatter + compute with overlap over the gr x gc block partition ``split``
+    (block_plan): every rank's input block travels as ``pieces`` consecutive row chunks
+    (separate point-to-point messages, in order), and ``compute(local, w_begin, w_end)``
+    runs for the block's window rows [w_begin, w_end) (block-relative) as soon as the
+    input rows they need, [w_begin, w_end + n0 - 1), have arrived — so rank g starts
+    after its first (short) chunk instead of after its whole block.  The sends go out
+    piece-major (one batched group per piece index: every peer's first chunk before any
+    peer's remainder).  A block narrower than the input is packed into a contiguous copy
+    per chunk on the source (row strips are sent as views).  The source rank computes
+    its own block at once, from a strided view of x.
+    Returns (local input block, (p0_begin, p0_end, p1_begin, p1_end, row_begin, row_end,
+    col_begin, col_end))."""
     rank = dist.get_rank(group)
     world = dist.get_world_size(group)
+    gr, gc = split
+    if gr * gc != world:
+        raise ValueError(f"split {gr}x{gc} does not cover {world} ranks")
     N0, N1 = int(shape[0]), int(shape[1])
-    n0 = 1 << m0
-    P0 = N0 - n0 + 1
-    plan = strip_plan(P0, m0, world)
-    a, b, rb, re = plan[rank]
+    n0, n1 = 1 << m0, 1 << m1
+    plan = block_plan(N0 - n0 + 1, N1 - n1 + 1, m0, m1, gr, gc)
+    mine = plan[rank]
+    a, b, _, _, rb, re, cb, ce = mine
     if rank == src:
         if x is None or tuple(x.shape) != (N0, N1):
             raise core.ShapeError(f"source rank needs the full {N0}x{N1} input")
-        works = []
-        for g, (ga, gb, grb, gre) in enumerate(plan):
-            if g == src or gre <= grb:
+        if x.stride(1) != 1 or (N0 > 1 and x.stride(0) != N1):
+            raise ValueError("the source input must be C-contiguous (rows are sent as views)")
+        per_peer = []  # (peer, [(first input row, end row) of each piece], cols)
+        for g, (ga, gb, _, _, grb, gre, gcb, gce) in enumerate(plan):
+            if g == src or gre <= grb or gce <= gcb:
                 continue
             wb = piece_bounds(gb - ga, first_fraction, pieces)
             cuts = [0] + [w + n0 - 1 for w in wb[1:-1]] + [gre - grb]
-            for c in range(len(cuts) - 1):  # in order: the peer computes piece c on arrival
-                works.append(dist.isend(x[grb + cuts[c]:grb + cuts[c + 1]].contiguous(), g,
-                                        group=group))
-        local = x[rb:re]
-        if b > a:
+            per_peer.append((g, [(grb + cuts[c], grb + cuts[c + 1]) for c in range(len(cuts) - 1)],
+                             (gcb, gce)))
+        # piece-major: one batched group per piece index, so every peer's (short) first
+        # chunk leaves before any peer's remainder, whatever stream(s) the backend runs
+        # its point-to-point operations on; within a peer, pieces arrive in order
+        works = []
+        for c in range(max((len(ps) for _, ps, _ in per_peer), default=0)):
+            ops = []
+            for g, ps, (gcb, gce) in per_peer:
+                if c < len(ps):
+                    t = x[ps[c][0]:ps[c][1], gcb:gce]
+                    ops.append(dist.P2POp(dist.isend, t if gce - gcb == N1 else t.contiguous(),
+                                          g, group))
+            works += dist.batch_isend_irecv(ops)
+        local = x[rb:re, cb:ce]
+        if b > a and ce > cb:
             compute(local, 0, b - a)
         for w in works:
             w.wait()
-        return local, (a, b, rb, re)
-    local = recv if recv is not None else torch.empty((re - rb, N1), dtype=dtype, device=device)
-    if tuple(local.shape) != (re - rb, N1):
-        raise ValueError(f"recv buffer must have shape {(re - rb, N1)}")
-    if b > a:
+        return local, mine
+    local = recv if recv is not None else torch.empty((re - rb, ce - cb), dtype=dtype,
+                                                      device=device)
+    if tuple(local.shape) != (re - rb, ce - cb):
+        raise ValueError(f"recv buffer must have shape {(re - rb, ce - cb)}")
+    if b > a and ce > cb:
         wb = piece_bounds(b - a, first_fraction, pieces)
         cuts = [0] + [w + n0 - 1 for w in wb[1:-1]] + [re - rb]
-        works = [dist.irecv(local[cuts[c]:cuts[c + 1]], src, group=group)
+        works = [dist.batch_isend_irecv([dist.P2POp(dist.irecv, local[cuts[c]:cuts[c + 1]], src,
+                                                    group)])
                  for c in range(len(cuts) - 1)]
         for c in range(len(wb) - 1):
-            works[c].wait()  # NCCL: the compute stream waits for this chunk only
+            for w in works[c]:
+                w.wait()  # NCCL: the compute stream waits for this chunk only
             compute(local, wb[c], wb[c + 1])
-    return local, (a, b, rb, re)
+    return local, mine
+
+
+def pipelined_strip_forward(x, shape, m0: int, dtype, device, compute, group=None, src: int = 0,
+                            recv=None, pieces: int = 2, first_fraction: float = 0.125):
+    """Row-strip form of pipelined_block_forward (split (world, 1), every rank all
+    columns).  Returns (local_rows_tensor, (p0_begin, p0_end, row_begin, row_end))."""
+    world = dist.get_world_size(group)
+    # m1 only sets the column halo, and a row strip has every column: pass m1 = 0
+    local, p = pipelined_block_forward(x, shape, m0, 0, (world, 1), dtype, device, compute,
+                                       group, src, recv, pieces, first_fraction)
+    return local, (p[0], p[1], p[4], p[5])
 
 
 def tree_swdft_2d_sharded(x, spec, *, shape=None, dtype=None, group=None, src: int = 0,

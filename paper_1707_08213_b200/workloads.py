@@ -51,13 +51,15 @@ class Workload:
     def in_bytes(self) -> int:
         return self.N0 * self.N1 * np.dtype(self.dtype).itemsize
 
-    def algorithmic_bytes(self, rows: int | None = None) -> int:
+    def algorithmic_bytes(self, rows: int | None = None, precision: str | None = None) -> int:
         """Output bytes written + input bytes read, for the
-        full output or for ``rows`` window rows."""
+        full output or for ``rows`` window rows, at the config's precision or
+        ``precision`` ("fp32": 8 B per coefficient, "fp64": 16 B)."""
+        ob = self.out_bytes_per_coef if precision is None else (16 if precision == "fp64" else 8)
         if rows is None:
-            return self.coefficients * self.out_bytes_per_coef + self.in_bytes
+            return self.coefficients * ob + self.in_bytes
         in_rows = rows + self.n0 - 1
-        return (rows * self.P1 * self.n0 * self.n1 * self.out_bytes_per_coef
+        return (rows * self.P1 * self.n0 * self.n1 * ob
                 + in_rows * self.N1 * np.dtype(self.dtype).itemsize)
 
     def generate(self, rows: int | None = None) -> np.ndarray:

@@ -2,10 +2,11 @@
 
     python scripts/ncu_summary.py --round r01 gpurun_out/prof_r01_c4.ncu-rep:c4:1024 ...
 
-Each argument is REPORT:CONFIG:ROWS (ROWS = window rows the capture launched, 0 = all).
-Writes profiles/ncu_<round>.md (human table) and merges per-config numbers into
-profiles/ncu_summary.json (read by bench.py for roofline.traffic when a full-launch
-capture exists).
+Each argument is REPORT:CONFIG:ROWS[:PREC] (ROWS = window rows the capture launched,
+0 = all; PREC = fp32 / fp64, default the config's precision).  Writes
+profiles/ncu_<round>.md (human table) and merges the numbers into
+profiles/ncu_summary.json under "<config>/<prec>" (read by bench.py for
+roofline.traffic when a full-launch capture of that config AND precision exists).
 """
 import argparse
 import csv
@@ -71,21 +72,23 @@ def traffic_table(paths):
             "write TB/s |", "|---|---|---|---|---|---|---|---|"]
     per_cfg = {}
     for spec in paths:
-        path, name = spec.split(":")
+        path, name, *pp = spec.split(":")
         cfg = CONFIGS[name]
+        prec = pp[0] if pp else cfg.precision
         lines = [l for l in open(path) if not l.startswith("==")]
         per = {}
         for row in csv.DictReader(lines):
             v = float(row["Metric Value"].replace(",", "")) * SCALE.get(row["Metric Unit"], 1.0)
             per.setdefault(int(row["ID"]), {})[row["Metric Name"]] = v
-        alg = cfg.algorithmic_bytes()
+        alg = cfg.algorithmic_bytes(precision=prec)
         for i, (_, m) in enumerate(sorted(per.items())):
             rd, wr = m["dram__bytes_read.sum"], m["dram__bytes_write.sum"]
             du = m["gpu__time_duration.sum"]
-            rows.append(f"| {name} | {i} | {du * 1e3:.3f} | {alg / 1e9:.3f} | {rd / 1e9:.4f} | "
+            rows.append(f"| {name} {prec} | {i} | {du * 1e3:.3f} | {alg / 1e9:.3f} | {rd / 1e9:.4f} | "
                         f"{wr / 1e9:.3f} | {(rd + wr) / alg:.4f} | "
                         f"{m.get('dram__bytes_write.sum.per_second', wr / du) / 1e12:.2f} |")
-            per_cfg[name] = {"dram_bytes_per_launch": rd + wr, "full_launch_duration_s": du}
+            per_cfg[f"{name}/{prec}"] = {"dram_bytes_per_launch": rd + wr,
+                                         "full_launch_duration_s": du}
     return rows, per_cfg
 
 
@@ -106,21 +109,22 @@ def main():
              "stall long-sb / barrier / short-sb (per issue) |",
              "|---|---|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for spec in a.captures:
-        rep, name, rows = spec.split(":")
+        rep, name, rows, *pp = spec.split(":")
         cfg = CONFIGS[name]
+        prec = pp[0] if pp else cfg.precision
         rows = int(rows) or cfg.P0
         for d in read_raw(rep):
-            alg = cfg.algorithmic_bytes(rows=rows)
+            alg = cfg.algorithmic_bytes(rows=rows, precision=prec)
             traffic = d.get("dram_read", 0) + d.get("dram_write", 0)
             lines.append(
-                f"| {name} | {rows} | {d['duration']*1e3:.3f} | {alg/1e9:.3f} | {traffic/1e9:.3f} | "
+                f"| {name} {prec} | {rows} | {d['duration']*1e3:.3f} | {alg/1e9:.3f} | {traffic/1e9:.3f} | "
                 f"{traffic/alg:.4f} | {d.get('dram_write_rate', 0)/1e12:.2f} | "
                 f"{d.get('dram_pct_of_peak', 0):.1f} | {d.get('sm_pct', 0):.1f} | "
                 f"{d.get('issue_pct', 0):.1f} | {d.get('fma_pipe_pct', 0):.1f} | {d.get('regs', 0):.0f} | "
                 f"{d.get('block', 0):.0f} x {d.get('grid', 0):.0f} | {d.get('occupancy_pct', 0):.1f} | "
                 f"{d.get('stall_long_sb', 0):.2f} / {d.get('stall_barrier', 0):.2f} / "
                 f"{d.get('stall_short_sb', 0):.2f} |")
-            e = summ.setdefault(name, {})
+            e = summ.setdefault(f"{name}/{prec}", {})
             e.update({"round": a.round, "capture_rows": rows, "duration_s": d["duration"],
                       "alg_bytes": alg, "traffic_bytes": traffic, "traffic_over_alg": traffic / alg})
             if rows == cfg.P0:

@@ -60,9 +60,27 @@ def _worker_pipelined(rank, world, port, m0, m1, shape, outdir, pieces):
             results[(w0, w1)] = oracle.tree2d(rows, m0, m1)
             calls.append((w0, w1))
 
-        local, (a, b, rb, re) = pipelined_strip_forward(x, shape, m0, torch.float64,
-                                                        torch.device("cpu"), compute,
-                                                        pieces=pieces, first_fraction=0.2)
+        groups = []  # rank 0: the (peer, rows) of each batched send group, in issue order
+        real = dist.batch_isend_irecv
+
+        def recording(ops):
+            groups.append([(op.peer, int(op.tensor.shape[0])) for op in ops])
+            return real(ops)
+
+        dist.batch_isend_irecv = recording
+        try:
+            local, (a, b, rb, re) = pipelined_strip_forward(x, shape, m0, torch.float64,
+                                                            torch.device("cpu"), compute,
+                                                            pieces=pieces, first_fraction=0.2)
+        finally:
+            dist.batch_isend_irecv = real
+        if rank == 0 and world > 1:
+            # piece-major: group c holds piece c of every peer that has one; group 0 has
+            # every peer with rows, so no peer's first chunk waits behind another's rest
+            peers0 = [g for g, _ in groups[0]]
+            assert peers0 == [g for g in range(1, world)], groups
+            for c, grp in enumerate(groups):
+                assert len({g for g, _ in grp}) == len(grp), groups
         if b > a:
             out = np.concatenate([results[k] for k in sorted(results)])
             np.save(os.path.join(outdir, f"p{rank}.npy"), out)
