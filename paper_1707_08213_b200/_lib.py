@@ -149,7 +149,7 @@ def workspace_bytes(N0: int, N1: int, m0: int, m1: int, prec: int, p0_begin: int
     return int(v.value)
 
 
-K1_MODES = {0: "uniform", 1: "guided", 2: "oneshot"}
+K1_MODES = {0: "uniform", 1: "guided", 2: "oneshot", 3: "streamk"}
 
 
 def k1_schedule(N0: int, N1: int, m0: int, m1: int, prec: int, p0_begin: int = 0,

@@ -54,6 +54,12 @@ static const int g_k1_oneshot = [] {
     const char *e = std::getenv("SWDFT2D_K1_ONESHOT");
     return e ? (e[0] == '1' ? 1 : 0) : -1;
 }();
+// K1 stream-K schedule: SWDFT2D_K1_STREAMK=k (k >= 1) forces equal contiguous shares of
+// the (column block, window row) space over k x slots CTAs, =0 never; unset = the rule
+static const int g_k1_streamk = [] {
+    const char *e = std::getenv("SWDFT2D_K1_STREAMK");
+    return e ? std::atoi(e) : -1;
+}();
 static const bool g_use_tma = [] {
     const char *e = std::getenv("SWDFT2D_TMA");
     return e && e[0] == '1';
@@ -407,7 +413,7 @@ static int select_path(int m0, int m1, int prec, int kernel, Path *path) {
 struct K1Plan {
     int occ = 0;
     int64_t slots = 0, grid = 0;
-    bool oneshot = false, guided = false;
+    bool oneshot = false, guided = false, streamk = false;
 };
 
 static int k1_plan(DeviceState *ds, const K1Info *k1, int64_t P1, int64_t p0_begin,
@@ -482,6 +488,40 @@ static int k1_plan(DeviceState *ds, const K1Info *k1, int64_t P1, int64_t p0_beg
     pl->oneshot = oneshot;
     pl->guided = guided;
     pl->grid = (oneshot || P->ntiles < slots) ? P->ntiles : slots;
+    // Stream-K (equal contiguous shares of the column-block-major row space, one
+    // tile per column block a share touches) where the tile grids above quantize badly
+    // (profiles/sched_sweep_r02*.jsonl, configs 2-5 and their 2-D partition blocks):
+    //  * uniform chunks: when a k = 1 share is >= 2 warm-ups (n0 - 1 rows), k = share /
+    //    (5 warm-ups) waves of CTAs, clamped to 1..4 (1 when one CTA fills an SM: the SM
+    //    idles between the CTAs of successive waves).  Config 2: 0.0983 -> 0.0932 ms
+    //    (k = 2); column blocks of config 4 (4081 x 511) +7-10 %, config 3 +4-8 %, 32x64 /
+    //    64x32 / 64x64 windows +4-22 %.
+    //  * one-shot grids whose last wave is < 90 % full (column blocks 3.4 x slots:
+    //    +11-13 % on config 5 blocks of 497 columns), k = 1.
+    // Guided schedules stay: long-lived stream-K CTAs spread their stores over the whole
+    // output, and on large outputs that measured 3-20 % slower than guided chunks.
+    int sk = g_k1_streamk;
+    if (sk < 0 && g_k1_oneshot < 0 && g_k1_guided < 0 && !std::getenv("SWDFT2D_K1_RCH")) {
+        const int64_t warm = n0 - 1 > 0 ? n0 - 1 : 1;
+        const double share = (double)P->CB * (double)rows / (double)slots;
+        sk = 0;
+        if (oneshot) {
+            const double waves = (double)P->CB / (double)slots;
+            if (waves / std::ceil(waves) < 0.9) sk = 1;
+        } else if (!guided && share >= 2.0 * (double)warm) {
+            const int k = (int)(share / (5.0 * (double)warm));
+            sk = pl->occ == 1 ? 1 : k < 1 ? 1 : k > 4 ? 4 : k;
+        }
+    }
+    if (sk > 0) {
+        const int64_t L = P->CB * rows;
+        pl->streamk = true;
+        pl->oneshot = pl->guided = false;
+        P->streamk = 1;
+        P->nchunks = 0;
+        pl->grid = (int64_t)sk * slots < L ? (int64_t)sk * slots : L;
+        P->ntiles = pl->grid;
+    }
     return SWDFT2D_OK;
 }
 
@@ -663,8 +703,8 @@ int swdft2d_k1_schedule(int64_t N0, int64_t N1, int m0, int m1, int prec, int64_
     K1Plan pl;
     if ((rc = k1_plan(ds, k1, P1, p0_begin, p0_end, &P, &pl))) return rc;
     const int64_t rows = p0_end - p0_begin;
-    const int64_t nchunks = P.nchunks > 0 ? P.nchunks : (rows + P.RCH - 1) / P.RCH;
-    info[0] = pl.oneshot ? 2 : pl.guided ? 1 : 0;
+    const int64_t nchunks = pl.streamk ? 0 : P.nchunks > 0 ? P.nchunks : (rows + P.RCH - 1) / P.RCH;
+    info[0] = pl.streamk ? 3 : pl.oneshot ? 2 : pl.guided ? 1 : 0;
     info[1] = P.RCH;
     info[2] = nchunks;
     info[3] = P.ntiles;

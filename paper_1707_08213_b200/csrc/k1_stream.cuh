@@ -163,17 +163,43 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
     for (int q = 0; q < S::RING; ++q) rring[q] = mk<T>(0, 0);
 
     __shared__ int64_t s_next;
-    for (int64_t tile = blockIdx.x; tile < P.ntiles;) {
-        const int64_t cb = tile % P.CB, rc = tile / P.CB;
-        const int64_t pbase = cb * TP1;
-        int64_t r0, r1;  // output rows [r0, r1)
-        if (P.nchunks > 0) {
-            r0 = P.p0_begin + P.chunk[rc];
-            r1 = P.p0_begin + P.chunk[rc + 1];
+    // stream-K: this CTA's share [lin, lin_end) of the column-block-major space in COST
+    // units — each column block is its n0 - 1 warm-up rows followed by its window rows —
+    // so a share that crosses into the next column block pays for that block's warm-up
+    // out of its share, and every CTA costs its share plus at most one warm-up of its own
+    const int64_t rows_all = P.p0_end - P.p0_begin;
+    const int64_t U = rows_all + (n0 - 1);
+    int64_t lin = 0, lin_end = 0;
+    if (P.streamk) {
+        const int64_t L = P.CB * U;
+        lin = (int64_t)blockIdx.x * L / gridDim.x;
+        lin_end = (int64_t)(blockIdx.x + 1) * L / gridDim.x;
+    }
+    for (int64_t tile = blockIdx.x;;) {
+        int64_t cb, r0, r1;  // column block, output rows [r0, r1)
+        if (P.streamk) {
+            if (lin >= lin_end) break;
+            cb = lin / U;
+            const int64_t cend = (cb + 1) * U;
+            const int64_t se = lin_end < cend ? lin_end : cend;
+            const int64_t a = lin - cb * U - (n0 - 1), e = se - cb * U - (n0 - 1);
+            lin = se;
+            if (e <= 0) continue;  // the share ends inside this block's warm-up: no rows
+            r0 = P.p0_begin + (a > 0 ? a : 0);
+            r1 = P.p0_begin + e;
         } else {
-            r0 = P.p0_begin + rc * P.RCH;
-            r1 = r0 + P.RCH < P.p0_end ? r0 + P.RCH : P.p0_end;
+            if (tile >= P.ntiles) break;
+            cb = tile % P.CB;
+            const int64_t rc = tile / P.CB;
+            if (P.nchunks > 0) {
+                r0 = P.p0_begin + P.chunk[rc];
+                r1 = P.p0_begin + P.chunk[rc + 1];
+            } else {
+                r0 = P.p0_begin + rc * P.RCH;
+                r1 = r0 + P.RCH < P.p0_end ? r0 + P.RCH : P.p0_end;
+            }
         }
+        const int64_t pbase = cb * TP1;
         const int64_t in_end = r1 + n0 - 1;                         // input rows [r0, in_end)
         const int nbatch = (int)((in_end - r0 + NB - 1) / NB);
         // Output addressing, kept off the per-row critical path: a running pointer to

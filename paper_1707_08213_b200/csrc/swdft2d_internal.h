@@ -41,6 +41,10 @@ struct K1Params {
     int nchunks;
     unsigned long long *counter;
     int64_t chunk[K1_MAX_CHUNKS + 1];
+    // stream-K schedule (streamk != 0): the CB x rows (column block, window row) space,
+    // column-block major, is cut into gridDim.x equal contiguous ranges; CTA b walks
+    // range b as one tile per column block it touches (each with its own warm-up)
+    int streamk;
     int sample_bytes;    // bytes per input sample (4, 8, 16)
     int tma_per_sample;  // TMA elements per sample (1, or 2 for complex128)
     int tma_row_bytes;   // bytes of one staged input row (TMA box width, 16-B multiple)

@@ -16,6 +16,9 @@ here:
   * the fp32 production schedules of configs 3-5 are bitwise equal to K1 re-run on
     short row ranges (other tiles, other warm-up rows: each node's arithmetic does
     not depend on the schedule);
+  * the stream-K schedule (equal contiguous shares of the column-block-major row space;
+    config 2, column blocks of config 4) in fp64, bitwise against KR + KC on every row
+    and the oracle around the rows where shares start;
   * the guided tile counter (one slot per stream, zeroed by each launch's last fetch)
     survives back-to-back launches and concurrent streams;
   * the randomised fuzz runs with the schedule overrides forced, so small shapes go
@@ -127,6 +130,44 @@ def test_config5_oneshot_fp64_bitwise(cuda, oracle_lib):
     torch.cuda.empty_cache()
 
 
+def streamk_share_rows(sched, rows, n0, picks=(1, 2)):
+    """Window rows where stream-K CTA shares begin inside a column block (CTA b's share
+    starts at b * L // grid of the column-block-major cost space, each column block
+    being n0 - 1 warm-up units followed by its rows; k1_stream.cuh)."""
+    U = rows + n0 - 1
+    L = sched["column_blocks"] * U
+    return [max(0, (b * L // sched["grid"]) % U - (n0 - 1))
+            for b in picks + (sched["grid"] // 2, sched["grid"] - 1)]
+
+
+@pytest.mark.parametrize("case", ["c2", "c4cols"])
+def test_streamk_production_schedule_fp64_bitwise(cuda, oracle_lib, case):
+    """The stream-K schedule (abi.cu k1_plan: uniform-chunk shapes whose shares span
+    >= 2 warm-ups — config 2 whole, and a column block of config 4 as a 1 x 8 partition
+    rank owns it) in fp64: every row bitwise against KR + KC, and oracle strips around
+    the rows where CTA shares start mid column block (each share starts its own warm-up)."""
+    cfg = CONFIGS["c2" if case == "c2" else "c4"]
+    x = cfg.generate()
+    if case == "c4cols":  # the largest column block of a 1 x 8 split: 511 window columns
+        x = np.ascontiguousarray(x[:, :511 + cfg.n1 - 1])
+    N0, N1 = x.shape
+    P0, P1 = N0 - cfg.n0 + 1, N1 - cfg.n1 + 1
+    xd = torch.from_numpy(x).to(cuda)
+    sched = _lib.k1_schedule(N0, N1, cfg.m0, cfg.m1, _lib.PREC_FP64)
+    assert sched["mode"] == "streamk", sched
+    out = torch.empty((P0, P1, cfg.n0, cfg.n1), dtype=torch.complex128, device=cuda)
+    forward_into(xd, cfg.m0, cfg.m1, out, prec=_lib.PREC_FP64)
+    assert compare_with_separable(xd, cfg, out, _lib.PREC_FP64) == []
+    threads = len(os.sched_getaffinity(0))
+    strip = 32
+    for r in sorted(set(streamk_share_rows(sched, P0, cfg.n0)) | {0, P0 - strip}):
+        a = max(0, min(P0 - strip, r - strip // 2))
+        ref = oracle_lib.tree2d(x[a:a + strip + cfg.n0 - 1], cfg.m0, cfg.m1, threads=threads)
+        assert bits_equal_np(out[a:a + strip].cpu().numpy(), ref), (case, a)
+    del out
+    torch.cuda.empty_cache()
+
+
 @pytest.mark.parametrize("name", ["c3", "c4", "c5"])
 def test_fp32_production_schedule_equals_short_launches(cuda, name):
     """fp32: the full-size production launch is bitwise equal to K1 over short row ranges
@@ -200,6 +241,9 @@ def test_guided_counter_reuse_and_concurrent_streams(cuda):
     {"SWDFT2D_K1_ONESHOT": "1", "SWDFT2D_K1_GUIDED": "1"},
     {"SWDFT2D_K1_RCH": "3"},
     {"SWDFT2D_K1_RCH": "3", "SWDFT2D_K1_GUIDED": "0"},
+    {"SWDFT2D_K1_STREAMK": "1"},
+    {"SWDFT2D_K1_STREAMK": "3"},
+    {"SWDFT2D_K1_STREAMK": "0"},
 ], ids=lambda e: ",".join(f"{k[10:]}={v}" for k, v in e.items()))
 def test_fuzz_under_schedule_overrides(env):
     r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "fuzz_parity.py"),
