@@ -248,8 +248,21 @@ def run_reference(args, cfg, rank):
     print(json.dumps(line), flush=True)
 
 
+def make_flush(dev):
+    """Two 256 MiB buffers (> the 126 MB L2): one written, one read by every flush."""
+    import torch
+
+    return (torch.empty(64 << 20, dtype=torch.float32, device=dev),
+            torch.ones(64 << 20, dtype=torch.float32, device=dev))
+
+
 def flush_l2(buf):
-    buf.fill_(1.0)
+    """Write 256 MiB (evicts the step's input and output from L2), then read another
+    256 MiB, so the step starts with a clean L2: after the write alone L2 held ~126 MB
+    of DIRTY flush lines whose write-back the next step's first stores paid for
+    (config 2: 0.0922 -> 0.0881 ms, profiles/flush_effect_r02.jsonl)."""
+    buf[0].fill_(1.0)
+    buf[1].sum()
 
 
 def run_ours(args, cfg, rank, world, local_rank):
@@ -267,7 +280,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     prec = _precision_code(args.precision or cfg.precision, None)
     odt = _OUT_DTYPES[prec]
     stream = torch.cuda.current_stream(dev)
-    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)  # 256 MiB > 126 MB L2
+    flush = make_flush(dev)  # 2 x 256 MiB > 126 MB L2
 
     # N > 1 modes: "weak" (default) — every rank transforms its own full workload (its
     # own share of window rows of an N-times taller array, generated locally): no
@@ -368,8 +381,9 @@ def run_ours(args, cfg, rank, world, local_rank):
         "config": {"workload": cfg.name, "desc": cfg.desc, "N0": cfg.N0, "N1": cfg.N1,
                    "window": [n0, n1], "coefficients": cfg.coefficients,
                    "output_bytes": cfg.coefficients * out_bpc,
-                   "l2": "256 MiB flush write before every timed step (queued ahead of the "
-                         "start event, outside the timed interval); output >> L2 as well",
+                   "l2": "L2 flushed before every timed step: 256 MiB written, then another "
+                         "256 MiB read so L2 starts clean (queued ahead of the start event, "
+                         "outside the timed interval); output >> L2 as well",
                    "parallelism": (f"strips{world} (NCCL scatter from rank 0)" if strips else
                                    f"replicas{world} (each rank its own full workload, no "
                                    "data-path collective)" if world > 1 else "single"),
@@ -430,7 +444,7 @@ def strong_detail(args, cfg, rank, world, dev, stream, x_full, recv, out, prec, 
     from paper_1707_08213_b200.partition import pipelined_strip_forward, strip_plan
     from paper_1707_08213_b200.tree2d import _OUT_DTYPES, forward_into
 
-    flush = torch.empty(64 << 20, dtype=torch.float32, device=dev)
+    flush = make_flush(dev)
     a, b, rb, re = strip_plan(cfg.P0, cfg.m0, world)[rank]
     xdt = x_full.dtype if x_full is not None else recv.dtype
     local = x_full[rb:re] if x_full is not None else recv

@@ -323,6 +323,16 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
             const C *zb = ring + (((b * NB) & (D - 1)) + D) * (TP1 * n1) + pos * n1 + k1;
 #pragma unroll 1
             for (int k0r = 0; k0r < NB; k0r += S::UNR) {
+                // Warm-up rows whose column-tree nodes no emitted row depends on: the
+                // level-l node of tile row rel feeds emitted rows (rel >= n0 - 1) only if
+                // rel >= n0 - n0/2^l, and stage C starts at level Q (rebuilt from the Z
+                // ring), so rows rel < n0 - n0/J need no stage C at all — only their Z rows
+                // (stage R above).  Later rows read the register ring only for such unused
+                // nodes, so skipping changes no emitted value (fp64 stays bitwise).
+                if (b * NB + k0r + S::UNR <= n0 - n0 / J) {
+                    orow += S::UNR * ostride;
+                    continue;
+                }
                 const C *zr = zb + k0r * (TP1 * n1);
                 static_for<S::UNR>([&](auto kuc) {
                     constexpr int ku = decltype(kuc)::value;

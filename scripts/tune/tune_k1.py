@@ -82,6 +82,7 @@ def run_variant(lib, v, name, cfg, cache, dev, flush, a):
         ts = []
         for _ in range(a.reps):
             flush.fill_(1.0)
+            torch.cuda._sleep(300000)  # the host enqueues the launch before e0 runs
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(s)
             launch()
