@@ -20,11 +20,13 @@ Default workload: config 4 (4096x4096 f32 image-like array, 16x16 windows,
              on the first window rows of the same config (rank 0, N=1 only)
 
 N > 1 (torchrun, one process per GPU, NCCL), --scaling strong (default): ONE
-workload partitioned into window-row strips, the north-star deployment; rank 0
-holds the input in HBM and each step = pipelined scatter of input row strips with
-their halos (NCCL send/recv from rank 0, piece-major: every rank's first chunk
-first) + every rank's strip of the transform; value = coefficients / (max over
-ranks of the step time).  The line's "strong" object adds the scatter alone, the
+workload partitioned into gr x gc blocks of window rows x window columns (gr = N,
+gc = 1 are the north star's window-row strips; the split is measured once on rank 0
+per shape and broadcast, partition.choose_split; --split forces one); rank 0 holds
+the input in HBM and each step = pipelined scatter of the input blocks with their
+halos (NCCL send/recv from rank 0, piece-major: every rank's first chunk first; a
+receiver's pieces alternate between two streams) + every rank's block of the
+transform; value = coefficients / (max over ranks of the step time).  The line's "strong" object adds the scatter alone, the
 compute alone and an in-run N=1 time of the same workload on rank 0, with
 E(N) = t(1) / (N t(N)).  --scaling weak: every rank transforms its own
 config-sized workload (generated locally) with no data-path collective.
@@ -271,7 +273,8 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     from paper_1707_08213_b200 import WindowSpec, tree_swdft_2d
     from paper_1707_08213_b200 import _lib
-    from paper_1707_08213_b200.partition import choose_pieces, pipelined_strip_forward, strip_plan
+    from paper_1707_08213_b200.partition import (block_plan, choose_pieces, choose_split,
+                                                  pipelined_block_forward)
     from paper_1707_08213_b200.tree2d import _OUT_DTYPES, _precision_code, forward_into
 
     torch.cuda.set_device(local_rank)
@@ -291,25 +294,34 @@ def run_ours(args, cfg, rank, world, local_rank):
     xdt = {"float32": torch.float32, "float64": torch.float64, "complex64": torch.complex64,
            "complex128": torch.complex128}[cfg.dtype]
     P0, P1, n0, n1 = cfg.P0, cfg.P1, cfg.n0, cfg.n1
-    plan = strip_plan(P0, cfg.m0, world if strips else 1)
-    a, b, rb, re = plan[rank if strips else 0]
-    out = torch.empty((b - a, P1, n0, n1), dtype=odt, device=dev)
     x_full = torch.from_numpy(x_np).to(dev) if x_np is not None else None
-    recv = torch.empty((re - rb, cfg.N1), dtype=xdt, device=dev) if x_full is None else None
-
-    pieces = choose_pieces((cfg.N0, cfg.N1), cfg.m0, cfg.m1, np.dtype(cfg.dtype).itemsize,
-                           out.element_size(), world) if strips else 1
+    # strong: the partition (gr x gc blocks of window rows x window columns) and the
+    # scatter's piece count are measured once on rank 0 and broadcast (choose_split);
+    # --split GRxGC forces one
+    split, pieces, split_table = (1, 1), 1, []
+    if strips:
+        if args.split:
+            split = tuple(int(v) for v in args.split.split("x"))
+            pieces = choose_pieces((cfg.N0, cfg.N1), cfg.m0, cfg.m1, np.dtype(cfg.dtype).itemsize,
+                                   8 if prec == _lib.PREC_FP32 else 16, world)
+        else:
+            ch = choose_split(x_full, (cfg.N0, cfg.N1), cfg.m0, cfg.m1, prec, world,
+                              np.dtype(cfg.dtype).itemsize)
+            split, pieces, split_table = tuple(ch["split"]), ch["pieces"], ch["table"]
+    a, b, c0, c1, rb, re, cb, ce = block_plan(P0, P1, cfg.m0, cfg.m1, *split)[rank if strips else 0]
+    out = torch.empty((b - a, c1 - c0, n0, n1), dtype=odt, device=dev)
+    recv = torch.empty((re - rb, ce - cb), dtype=xdt, device=dev) if x_full is None else None
 
     def compute(local, w0, w1):
-        forward_into(local, cfg.m0, cfg.m1, out[w0:w1], prec=prec, p0_begin=w0, p0_end=w1,
-                     stream=stream)
+        # on torch's current stream: the receive path alternates pieces between streams
+        forward_into(local, cfg.m0, cfg.m1, out[w0:w1], prec=prec, p0_begin=w0, p0_end=w1)
 
     def step():
-        # strong: the partitioner's pipelined scatter — every strip travels from rank 0 in
+        # strong: the partitioner's pipelined scatter — every block travels from rank 0 in
         # in-order chunks and each rank starts on its first chunk on arrival
         if strips:
-            pipelined_strip_forward(x_full if rank == 0 else None, (cfg.N0, cfg.N1), cfg.m0, xdt,
-                                    dev, compute, recv=recv, pieces=pieces)
+            pipelined_block_forward(x_full if rank == 0 else None, (cfg.N0, cfg.N1), cfg.m0,
+                                    cfg.m1, split, xdt, dev, compute, recv=recv, pieces=pieces)
         elif b > a:
             compute(x_full, 0, b - a)
 
@@ -384,10 +396,14 @@ def run_ours(args, cfg, rank, world, local_rank):
                    "l2": "L2 flushed before every timed step: 256 MiB written, then another "
                          "256 MiB read so L2 starts clean (queued ahead of the start event, "
                          "outside the timed interval); output >> L2 as well",
-                   "parallelism": (f"strips{world} (NCCL scatter from rank 0)" if strips else
+                   "parallelism": (f"blocks{split[0]}x{split[1]} (window rows x window "
+                                   "columns, NCCL scatter from rank 0)" if strips else
                                    f"replicas{world} (each rank its own full workload, no "
                                    "data-path collective)" if world > 1 else "single"),
-                   "scatter_pieces": pieces},
+                   "scatter_pieces": pieces,
+                   **({"split_choice": [{k: (list(v) if isinstance(v, tuple) else v)
+                                         for k, v in r.items()} for r in split_table]}
+                      if split_table else {})},
         "hbm_write_gbs": units * out_bpc / step_s / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak,
@@ -404,7 +420,7 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     if strips and not args.no_strong_detail:
         line["strong"] = strong_detail(args, cfg, rank, world, dev, stream, x_full, recv, out,
-                                       prec, pieces, step_s, graph_free=True)
+                                       prec, pieces, step_s, split, graph_free=True)
 
     # e2e through the public API from pinned host memory
     if not args.no_e2e:
@@ -413,7 +429,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         else:
             out = None
             torch.cuda.empty_cache()
-            line["e2e"] = e2e_sharded(args, cfg, x_np, dev, spec, xdt, prec, rank, world)
+            line["e2e"] = e2e_sharded(args, cfg, x_np, dev, spec, xdt, prec, rank, world, split,
+                                      pieces)
     if world == 1 and not args.no_others:
         graph = out = None
         torch.cuda.empty_cache()
@@ -433,21 +450,21 @@ def run_ours(args, cfg, rank, world, local_rank):
 
 
 def strong_detail(args, cfg, rank, world, dev, stream, x_full, recv, out, prec, pieces, step_s,
-                  graph_free=True):
+                  split, graph_free=True):
     """Strong-scaling breakdown (max over ranks, device-timed, L2 flushed): the pipelined
-    scatter alone (compute replaced by nothing), each rank's strip transform alone (input
+    scatter alone (compute replaced by nothing), each rank's block transform alone (input
     already resident), and t(1) = the whole workload on rank 0 alone in the same run, so
     E(N) = t(1) / (N t(N)) needs no other run."""
     import torch
     import torch.distributed as dist
 
-    from paper_1707_08213_b200.partition import pipelined_strip_forward, strip_plan
+    from paper_1707_08213_b200.partition import block_plan, pipelined_block_forward
     from paper_1707_08213_b200.tree2d import _OUT_DTYPES, forward_into
 
     flush = make_flush(dev)
-    a, b, rb, re = strip_plan(cfg.P0, cfg.m0, world)[rank]
+    a, b, c0, c1, rb, re, cb, ce = block_plan(cfg.P0, cfg.P1, cfg.m0, cfg.m1, *split)[rank]
     xdt = x_full.dtype if x_full is not None else recv.dtype
-    local = x_full[rb:re] if x_full is not None else recv
+    local = x_full[rb:re, cb:ce] if x_full is not None else recv
 
     def timed(fn, reps):
         ts = []
@@ -466,11 +483,11 @@ def strong_detail(args, cfg, rank, world, dev, stream, x_full, recv, out, prec, 
         return float(t.item())
 
     def scatter_only():
-        pipelined_strip_forward(x_full if rank == 0 else None, (cfg.N0, cfg.N1), cfg.m0, xdt,
-                                dev, lambda *_: None, recv=recv, pieces=pieces)
+        pipelined_block_forward(x_full if rank == 0 else None, (cfg.N0, cfg.N1), cfg.m0, cfg.m1,
+                                split, xdt, dev, lambda *_: None, recv=recv, pieces=pieces)
 
     def compute_only():
-        if b > a:
+        if b > a and c1 > c0:
             forward_into(local, cfg.m0, cfg.m1, out, prec=prec, p0_begin=0, p0_end=b - a,
                          stream=stream)
 
@@ -492,7 +509,7 @@ def strong_detail(args, cfg, rank, world, dev, stream, x_full, recv, out, prec, 
     torch.cuda.empty_cache()
     return {"t1_ms": t1 * 1e3, "tN_ms": step_s * 1e3, "efficiency_in_run": t1 / (world * step_s),
             "scatter_only_ms": t_scatter * 1e3, "compute_only_ms": t_compute * 1e3,
-            "scatter_pieces": pieces,
+            "scatter_pieces": pieces, "split": list(split),
             "note": "max over ranks, median of %d; t1 = whole workload on rank 0 alone, same run" % reps}
 
 
@@ -553,20 +570,20 @@ def other_configs(args, main_cfg, dev, flush, stream):
     return res
 
 
-def e2e_sharded(args, cfg, x_np, dev, spec, xdt, prec, rank, world):
+def e2e_sharded(args, cfg, x_np, dev, spec, xdt, prec, rank, world, split, pieces):
     """N > 1: rank 0's pinned host input -> H2D -> tree_swdft_2d_sharded (pipelined NCCL
-    scatter + K1 per strip) -> every rank copies its strip of coefficients to its own
+    scatter + K1 per block) -> every rank copies its block of coefficients to its own
     pinned host buffer (each GPU's own PCIe link).  Time = max over ranks."""
     import torch
     import torch.distributed as dist
 
-    from paper_1707_08213_b200.partition import strip_plan, tree_swdft_2d_sharded
+    from paper_1707_08213_b200.partition import block_plan, tree_swdft_2d_sharded
 
-    a, b, _, _ = strip_plan(cfg.P0, cfg.m0, world)[rank]
+    a, b, c0, c1 = block_plan(cfg.P0, cfg.P1, cfg.m0, cfg.m1, *split)[rank][:4]
     x_pin = torch.from_numpy(x_np).pin_memory() if rank == 0 else None
     from paper_1707_08213_b200.tree2d import _OUT_DTYPES
 
-    host_out = torch.empty((b - a, cfg.P1, cfg.n0, cfg.n1), dtype=_OUT_DTYPES[prec],
+    host_out = torch.empty((b - a, c1 - c0, cfg.n0, cfg.n1), dtype=_OUT_DTYPES[prec],
                            pin_memory=True)
     stream = torch.cuda.current_stream(dev)
     times = []
@@ -578,7 +595,8 @@ def e2e_sharded(args, cfg, x_np, dev, spec, xdt, prec, rank, world):
         e0.record(stream)
         xd = x_pin.to(dev, non_blocking=True) if rank == 0 else None
         sh = tree_swdft_2d_sharded(xd, spec, shape=(cfg.N0, cfg.N1), dtype=xdt,
-                                   precision="fp32" if prec == 0 else "fp64", budget=1 << 62)
+                                   precision="fp32" if prec == 0 else "fp64", budget=1 << 62,
+                                   split=split, pieces=pieces)
         host_out.copy_(sh.values, non_blocking=True)
         e1.record(stream)
         torch.cuda.synchronize()
@@ -594,7 +612,7 @@ def e2e_sharded(args, cfg, x_np, dev, spec, xdt, prec, rank, world):
     return {"value": cfg.coefficients / s, "unit": UNIT,
             "h2d_bytes_per_step": int(cfg.in_bytes), "d2h_bytes_per_step": int(d2h.item()),
             "ms_per_step": s * 1e3, "steps": len(times),
-            "path": "rank 0 pinned host input -> tree_swdft_2d_sharded -> each rank's strip "
+            "path": "rank 0 pinned host input -> tree_swdft_2d_sharded -> each rank's block "
                     "to its own pinned host buffer; max over ranks"}
 
 
@@ -700,6 +718,9 @@ def main():
     ap.add_argument("--strips", action="store_true",
                     help="run the strip path (pipelined scatter + per-strip K1) even at N=1 "
                          "(under torchrun; exercises the N>1 code on one GPU)")
+    ap.add_argument("--split", default=None,
+                    help="N>1 strong: force the GRxGC block partition (default: measured on "
+                         "rank 0 per shape, partition.choose_split)")
     ap.add_argument("--no-strong-detail", action="store_true",
                     help="N>1 strong: skip the scatter-only / compute-only / t(1) breakdown")
     ap.add_argument("--scaling", default="strong", choices=["weak", "strong"],

@@ -141,6 +141,101 @@ def choose_pieces(shape, m0: int, m1: int, in_bytes: int, out_bytes: int, world:
     return 2 if send_all - send_first > (n0 - 1) * row_t + 5e-6 else 1
 
 
+def split_candidates(world: int):
+    """Every gr x gc factorisation of ``world``, row strips (world x 1) first."""
+    return [(gr, world // gr) for gr in range(world, 0, -1) if world % gr == 0]
+
+
+_SPLITS: dict = {}
+
+
+def _block_area(p):
+    return max(0, p[1] - p[0]) * max(0, p[3] - p[2])
+
+
+def tune_split(x, m0: int, m1: int, prec: int, world: int, reps: int = 2):
+    """Measure on x's device which gr x gc partition of ``world`` ranks finishes first.
+
+    For every factorisation, K1 transforms the largest block a rank would own (from a
+    strided view of x, as the source rank does) — the per-block time includes its
+    schedule's wave quantization, warm-up rows and launch — and the scatter is added from
+    the bytes rank 0 sends at NVLINK_PEER_BPS: all of it (one piece) or only the first
+    pieces (two pieces, the rest hidden behind compute) when the second launch's extra
+    warm-up costs less than the transfer it hides.  Measured on one GPU the same way in
+    scripts/split_scaling.py (profiles/split_scaling_r02*.jsonl).  Returns {"split":
+    (gr, gc), "pieces": p, "table": [...]}."""
+    from .tree2d import _OUT_DTYPES, forward_into
+
+    N0, N1 = int(x.shape[0]), int(x.shape[1])
+    n0, n1 = 1 << m0, 1 << m1
+    P0, P1 = N0 - n0 + 1, N1 - n1 + 1
+    esz = x.element_size()
+    cands = []
+    for gr, gc in split_candidates(world):
+        plan = block_plan(P0, P1, m0, m1, gr, gc)
+        cands.append(((gr, gc), plan, max(plan, key=_block_area)))
+    most = max(_block_area(big) for _, _, big in cands) * n0 * n1
+    scratch = torch.empty(max(most, 1), dtype=_OUT_DTYPES[prec], device=x.device)
+    table = []
+    for split, plan, big in cands:
+        a0, b0, a1, b1, rb, re, cb, ce = big
+        if _block_area(big) == 0:
+            continue
+        view = x[rb:re, cb:ce]
+        o = scratch[:_block_area(big) * n0 * n1].view(b0 - a0, b1 - a1, n0, n1)
+        forward_into(view, m0, m1, o, prec=prec)
+        ts_ = []
+        for _ in range(reps):
+            torch.cuda.synchronize(x.device)
+            if hasattr(torch.cuda, "_sleep"):
+                torch.cuda._sleep(100000)  # host submission stays outside the events
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            forward_into(view, m0, m1, o, prec=prec)
+            e1.record()
+            e1.synchronize()
+            ts_.append(e0.elapsed_time(e1) / 1e3)
+        t = min(ts_)
+        send = first = 0
+        for g, p in enumerate(plan):
+            if g == 0 or _block_area(p) == 0:
+                continue
+            rows_in, cols_in = p[5] - p[4], p[7] - p[6]
+            send += rows_in * cols_in * esz
+            first += min(rows_in, piece_bounds(p[1] - p[0], 0.125, 2)[1] + n0 - 1) * cols_in * esz
+        t_all, t_first = send / NVLINK_PEER_BPS, first / NVLINK_PEER_BPS
+        # a second piece re-runs part of the n0 - 1 warm-up (about half of it: stage C is
+        # skipped on most warm-up rows) and adds a launch
+        extra = 0.5 * (n0 - 1) / max(1, b0 - a0) * t + 5e-6
+        pieces = 2 if t_all - t_first > extra else 1
+        score = t + (t_first + extra if pieces == 2 else t_all)
+        table.append({"split": split, "block": [b0 - a0, b1 - a1], "compute_s": t,
+                      "scatter_s": t_all, "pieces": pieces, "score_s": score})
+    del scratch
+    best = min(table, key=lambda r: r["score_s"])
+    return {"split": best["split"], "pieces": best["pieces"], "table": table}
+
+
+def choose_split(x, shape, m0: int, m1: int, prec: int, world: int, in_bytes: int,
+                 group=None, src: int = 0) -> dict:
+    """The partition every rank uses: measured once on ``src`` (tune_split), broadcast to
+    the group, cached per (shape, window, precision, world, element size) on every rank.
+    ``x`` is only read on ``src``."""
+    key = (tuple(int(v) for v in shape), int(m0), int(m1), int(prec), int(world), int(in_bytes))
+    hit = _SPLITS.get(key)
+    if hit is not None:
+        return hit
+    if world == 1:
+        res = {"split": (1, 1), "pieces": 1, "table": []}
+    else:
+        obj = [tune_split(x, m0, m1, prec, world) if dist.get_rank(group) == src else None]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, src) if group else src,
+                                   group=group)
+        res = obj[0]
+    _SPLITS[key] = res
+    return res
+
+
 def pipelined_block_forward(x, shape, m0: int, m1: int, split, dtype, device, compute,
                             group=None, src: int = 0, recv=None, pieces: int = 2,
                             first_fraction: float = 0.125):
@@ -207,11 +302,42 @@ def pipelined_block_forward(x, shape, m0: int, m1: int, split, dtype, device, co
         works = [dist.batch_isend_irecv([dist.P2POp(dist.irecv, local[cuts[c]:cuts[c + 1]], src,
                                                     group)])
                  for c in range(len(cuts) - 1)]
+        # On CUDA the pieces alternate between the current stream and a side stream, so a
+        # later piece's CTAs fill SMs as the previous piece's retire instead of waiting
+        # for its last CTA (scripts/split_scaling.py: "pipe2" vs "pipe1"); the current
+        # stream joins the side stream at the end.  compute() runs on torch's current stream.
+        cur = torch.cuda.current_stream(device) if device.type == "cuda" else None
+        side = _side_stream(device) if cur is not None and len(wb) > 2 else None
+        if side is not None:
+            side.wait_stream(cur)
         for c in range(len(wb) - 1):
-            for w in works[c]:
-                w.wait()  # NCCL: the compute stream waits for this chunk only
-            compute(local, wb[c], wb[c + 1])
+            st = side if side is not None and c % 2 == 1 else cur
+            with torch.cuda.stream(st) if st is not None else _nullctx():
+                for w in works[c]:
+                    w.wait()  # NCCL: the compute stream waits for this chunk only
+                compute(local, wb[c], wb[c + 1])
+        if side is not None:
+            cur.wait_stream(side)
     return local, mine
+
+
+_SIDE = {}
+
+
+def _side_stream(device):
+    """One side stream per device for the pipelined receive path."""
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    if idx not in _SIDE:
+        _SIDE[idx] = torch.cuda.Stream(torch.device("cuda", idx))
+    return _SIDE[idx]
+
+
+class _nullctx:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *exc):
+        return False
 
 
 def pipelined_strip_forward(x, shape, m0: int, dtype, device, compute, group=None, src: int = 0,
@@ -226,15 +352,19 @@ def pipelined_strip_forward(x, shape, m0: int, dtype, device, compute, group=Non
 
 
 def tree_swdft_2d_sharded(x, spec, *, shape=None, dtype=None, group=None, src: int = 0,
-                          precision=None, budget=None, pieces=None) -> ShardedCoefficients:
-    """Strip-sharded tree_swdft_2d: every rank returns its own window rows.
+                          precision=None, budget=None, pieces=None,
+                          split="auto") -> ShardedCoefficients:
+    """Sharded tree_swdft_2d: every rank returns its own block of the output.
 
     On ``src`` pass the full input tensor (CUDA); elsewhere pass x=None plus
-    ``shape`` and ``dtype``.  Budget accounting is the reference's, per strip.
+    ``shape`` and ``dtype``.  ``split``: "auto" (measured on ``src`` once per shape and
+    broadcast, choose_split), "strips" (window-row strips, world x 1) or an explicit
+    (gr, gc).  Budget accounting is the reference's, per block.
     """
     from .tree2d import _OUT_DTYPES, _precision_code, forward_into
 
     rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
     if rank == src:
         shape = tuple(int(s) for s in x.shape)
         dtype = x.dtype
@@ -248,22 +378,32 @@ def tree_swdft_2d_sharded(x, spec, *, shape=None, dtype=None, group=None, src: i
     prec = _precision_code(precision, dtype)
     n0, n1 = 1 << m0, 1 << m1
     P0, P1 = shape[0] - n0 + 1, shape[1] - n1 + 1
-    a, b, rb, re = strip_plan(P0, m0, dist.get_world_size(group))[dist.get_rank(group)]
-    if b > a:
-        sshape = (re - rb, shape[1])
-        core.check_budget(core.lattice_bytes(sshape, spec) + core.output_bytes(sshape, spec),
+    in_bytes = torch.empty((), dtype=dtype).element_size()
+    if split == "auto":
+        ch = choose_split(x if rank == src else None, shape, m0, m1, prec, world, in_bytes,
+                          group, src)
+        split = tuple(ch["split"])
+        if pieces is None:
+            pieces = ch["pieces"]
+    elif split in (None, "strips"):
+        split = (world, 1)
+    gr, gc = split
+    a, b, c0, c1, rb, re, cb, ce = block_plan(P0, P1, m0, m1, gr, gc)[rank]
+    if b > a and c1 > c0:
+        bshape = (re - rb, ce - cb)
+        core.check_budget(core.lattice_bytes(bshape, spec) + core.output_bytes(bshape, spec),
                           budget, what="level buffers + coefficient output")
-    out = torch.empty((b - a, P1, n0, n1), dtype=_OUT_DTYPES[prec], device=device)
+    out = torch.empty((b - a, c1 - c0, n0, n1), dtype=_OUT_DTYPES[prec], device=device)
     scale = core.normalization_factor(spec)
     if pieces is None:
-        pieces = choose_pieces(shape, m0, m1, torch.empty((), dtype=dtype).element_size(),
-                               out.element_size(), dist.get_world_size(group))
+        pieces = choose_pieces(shape, m0, m1, in_bytes, out.element_size(), world)
 
     def compute(local, w0, w1):
         forward_into(local, m0, m1, out[w0:w1], prec=prec, scale=scale, p0_begin=w0, p0_end=w1)
 
-    pipelined_strip_forward(x, shape, m0, dtype, device, compute, group, src, pieces=pieces)
-    return ShardedCoefficients(out, a, b, tuple(shape), spec, spec.normalization)
+    pipelined_block_forward(x, shape, m0, m1, split, dtype, device, compute, group, src,
+                            pieces=pieces)
+    return ShardedCoefficients(out, a, b, tuple(shape), spec, spec.normalization, c0, c1)
 
 
 def tree_swdft_2d_multi(x, spec, devices, *, precision=None, budget=None):

@@ -275,6 +275,50 @@ def test_strip_partition_on_device(cuda, world):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("split", [(2, 2), (1, 4), (4, 2), (1, 8), (3, 1)])
+def test_block_partition_on_device(cuda, split):
+    """Each rank's 2-D block (window rows x window columns + n0-1 halo rows and n1-1 halo
+    columns, partition.block_plan) computed alone — from a strided view of x, as the
+    source rank does, and from a packed copy, as a receiver does — reproduces its block
+    of the full output bitwise (fp64); the blocks tile the output exactly."""
+    from paper_1707_08213_b200.partition import block_plan
+
+    rng = np.random.default_rng(sum(split))
+    x = rng.standard_normal((75, 83))
+    m0, m1 = 3, 2
+    xt = torch.from_numpy(x).to(cuda)
+    P0, P1 = 75 - 7, 83 - 3
+    full = torch.empty((P0, P1, 8, 4), dtype=torch.complex128, device=cuda)
+    forward_into(xt, m0, m1, full, prec=_lib.PREC_FP64)
+    covered = np.zeros((P0, P1), dtype=int)
+    for (a, b, c0, c1, rb, re, cb, ce) in block_plan(P0, P1, m0, m1, *split):
+        covered[a:b, c0:c1] += 1
+        if b <= a or c1 <= c0:
+            continue
+        assert (re - rb, ce - cb) == (b - a + 7, c1 - c0 + 3)
+        for src in (xt[rb:re, cb:ce], xt[rb:re, cb:ce].clone()):
+            part = torch.empty((b - a, c1 - c0, 8, 4), dtype=torch.complex128, device=cuda)
+            forward_into(src, m0, m1, part, prec=_lib.PREC_FP64)
+            assert torch.equal(part.view(torch.float64), full[a:b, c0:c1].view(torch.float64))
+    assert (covered == 1).all()
+
+
+@pytest.mark.gpu
+def test_tune_split_measures_every_factorisation(cuda):
+    """partition.tune_split times the largest block of every gr x gc factorisation and
+    returns the lowest modelled step time."""
+    from paper_1707_08213_b200.partition import split_candidates, tune_split
+
+    x = torch.from_numpy(np.random.default_rng(3).standard_normal((300, 260))
+                         .astype(np.float32)).to(cuda)
+    res = tune_split(x, 4, 3, _lib.PREC_FP32, 4)
+    assert [tuple(r["split"]) for r in res["table"]] == split_candidates(4)
+    best = min(res["table"], key=lambda r: r["score_s"])
+    assert tuple(res["split"]) == tuple(best["split"]) and res["pieces"] in (1, 2)
+    assert all(r["compute_s"] > 0 and r["scatter_s"] > 0 for r in res["table"])
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("slots,dtype", [(1, np.float64), (3, np.float64), (8, np.float32),
                                          (4, np.complex128)])
 def test_forward_multi_slots(cuda, oracle_lib, slots, dtype):
@@ -358,8 +402,12 @@ def test_sharded_api_world1(cuda):
         x = torch.from_numpy(np.random.default_rng(8).standard_normal((60, 50))).to(cuda)
         sh = tree_swdft_2d_sharded(x, WindowSpec((3, 2), "unitary"), precision="fp64")
         ref = tree_swdft_2d(x, WindowSpec((3, 2), "unitary"), precision="fp64").values
-        assert (sh.p0_begin, sh.p0_end) == (0, 53)
+        assert (sh.p0_begin, sh.p0_end, sh.p1_begin, sh.p1_end) == (0, 53, 0, 47)
         assert torch.equal(sh.values.view(torch.float64), ref.view(torch.float64))
+        for split in ("strips", (1, 1)):
+            sh = tree_swdft_2d_sharded(x, WindowSpec((3, 2), "unitary"), precision="fp64",
+                                       split=split, pieces=2)
+            assert torch.equal(sh.values.view(torch.float64), ref.view(torch.float64))
     finally:
         dist.destroy_process_group()
 

@@ -131,3 +131,73 @@ def test_gloo_strip_scatter(tmp_path, world, shape, m):
             assert np.array_equal(part.view(np.uint64), full[a:b].view(np.uint64))
             rows.append((a, b))
     assert rows[0][0] == 0 and rows[-1][1] == full.shape[0]
+
+
+def _worker_blocks(rank, world, port, m0, m1, shape, split, pieces, outdir):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        from paper_1707_08213_b200 import partition
+
+        # choose_split: the source's measurement (stubbed: no GPU here) reaches every rank
+        # through the broadcast and is cached per shape, so a second call sends nothing
+        calls = []
+
+        def fake_tune(x, m0_, m1_, prec, w):
+            calls.append(1)
+            return {"split": split, "pieces": pieces, "table": [{"split": split}]}
+
+        partition.tune_split = fake_tune
+        ch = partition.choose_split(None, shape, m0, m1, 1, world, 8)
+        assert tuple(ch["split"]) == tuple(split) and ch["pieces"] == pieces
+        assert partition.choose_split(None, shape, m0, m1, 1, world, 8) is ch
+        assert len(calls) == (1 if rank == 0 else 0)
+
+        x = None
+        if rank == 0:
+            x = torch.from_numpy(np.random.default_rng(77).standard_normal(shape))
+        n0 = 1 << m0
+        results = {}
+
+        def compute(local, w0, w1):
+            results[(w0, w1)] = oracle.tree2d(local[w0:w1 + n0 - 1].numpy(), m0, m1)
+
+        local, (a, b, c0, c1, rb, re, cb, ce) = partition.pipelined_block_forward(
+            x, shape, m0, m1, split, torch.float64, torch.device("cpu"), compute, pieces=pieces)
+        assert tuple(local.shape) == (re - rb, ce - cb)
+        np.save(os.path.join(outdir, f"x{rank}.npy"), local.numpy())
+        if b > a and c1 > c0:
+            np.save(os.path.join(outdir, f"b{rank}.npy"),
+                    np.concatenate([results[k] for k in sorted(results)]))
+        with open(os.path.join(outdir, f"b{rank}.txt"), "w") as f:
+            f.write(f"{a} {b} {c0} {c1} {rb} {re} {cb} {ce}")
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,split,pieces,shape,m", [(4, (2, 2), 2, (40, 37), (3, 2)),
+                                                        (2, (1, 2), 1, (21, 30), (2, 3)),
+                                                        (3, (1, 3), 2, (19, 44), (3, 1))])
+def test_gloo_block_scatter(tmp_path, world, split, pieces, shape, m):
+    """2-D blocks (window rows x window columns with both halos) scattered from rank 0 in
+    pieces, the split broadcast from rank 0 by choose_split: every received block is the
+    right slice of x and the blocks' transforms tile the full output bitwise."""
+    import oracle
+
+    oracle.build()
+    port = _free_port()
+    mp.spawn(_worker_blocks, args=(world, port, m[0], m[1], shape, split, pieces, str(tmp_path)),
+             nprocs=world, join=True)
+    x = np.random.default_rng(77).standard_normal(shape)
+    full = oracle.tree2d(x, *m)
+    covered = np.zeros(full.shape[:2], dtype=int)
+    for r in range(world):
+        a, b, c0, c1, rb, re, cb, ce = map(int, open(tmp_path / f"b{r}.txt").read().split())
+        assert np.array_equal(np.load(tmp_path / f"x{r}.npy"), x[rb:re, cb:ce])
+        if b > a and c1 > c0:
+            part = np.load(tmp_path / f"b{r}.npy")
+            assert np.array_equal(part.view(np.uint64), full[a:b, c0:c1].view(np.uint64))
+            covered[a:b, c0:c1] += 1
+    assert (covered == 1).all()
