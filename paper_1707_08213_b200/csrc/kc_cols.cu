@@ -16,7 +16,16 @@
 
 namespace swdft2d {
 
-constexpr int KC_THREADS = 256;
+// CTA sizes: two 113 KB CTAs per SM of KC_THREADS_STD threads, or one 227 KB CTA (deep
+// tiles of n0 >= 512) of KC_THREADS_BIG threads — the passes are loops over thousands of
+// independent items, and a lone 256-thread CTA left the SM at 8 warps, latency-bound
+// (ncu, 1024 x 8: issue 35 %, profiles/ncu_r02.md)
+#ifndef KC_THREADS_STD
+#define KC_THREADS_STD 256
+#endif
+#ifndef KC_THREADS_BIG
+#define KC_THREADS_BIG 1024
+#endif
 constexpr size_t KC_SMEM_CAP = 113 * 1024;  // two CTAs per SM
 
 // nodes of level t for TP0 window rows: (TP0 + s_t - 1) 2^t, per column
@@ -37,8 +46,18 @@ __host__ __device__ constexpr int64_t kc_buf(int M0, int TP0, int which) {
     }
     return best;
 }
+// twiddles: Omega_n0[k] (n0 entries), then compact level tables Omega_L[k] = Omega_n0[k n0/L]
+// for L = 2 .. n0/4 at offset L - 2 (n0/2 - 2 entries): a pass reads level-L twiddles of
+// consecutive k, which at stride n0/L >= 4 in the n0 table all fell in one bank
+__host__ __device__ constexpr int kc_tw_entries(int M0) {
+    return (1 << M0) + (M0 >= 3 ? (1 << (M0 - 1)) - 2 : 0);
+}
 __host__ __device__ constexpr size_t kc_smem(int M0, int TP0, int CW, int esz) {
-    return (size_t)esz * ((size_t)CW * (kc_buf(M0, TP0, 0) + kc_buf(M0, TP0, 1)) + (1u << M0));
+    return (size_t)esz * ((size_t)CW * (kc_buf(M0, TP0, 0) + kc_buf(M0, TP0, 1)) + kc_tw_entries(M0));
+}
+// level-(l) twiddle k (Omega_{2^l}[k]) from the smem tables above
+template <int M0, typename C> __device__ __forceinline__ C kc_tw(const C *stw, int l, int k) {
+    return M0 - l <= 1 ? stw[k << (M0 - l)] : stw[(1 << M0) + (1 << l) - 2 + k];
 }
 // Tile shape (CW columns x TP0 window rows) within the cap, two rules:
 //  * wide (DEEP = false): the widest column group, then the most window rows — long
@@ -83,9 +102,10 @@ template <typename T, int M0, bool DEEP> struct KCShape {
     }
     static constexpr int CW = pick(0), TP0 = pick(1);
     static constexpr size_t SMEM = kc_smem(M0, TP0, CW, (int)sizeof(T) * 2);
+    static constexpr int THREADS = CAP > KC_SMEM_CAP ? KC_THREADS_BIG : KC_THREADS_STD;
 };
 
-template <typename T, bool EXACT, int M0, int TP0, int CW, int t, bool LAST>
+template <typename T, bool EXACT, int M0, int TP0, int CW, int t, bool LAST, int KC_THREADS>
 __device__ __forceinline__ void kc_pass4(const cplx<T> *src, cplx<T> *dst, const cplx<T> *stw,
                                          int npos, int ncol, const KCParams &P, int64_t r0,
                                          int64_t c0) {
@@ -94,19 +114,32 @@ __device__ __forceinline__ void kc_pass4(const cplx<T> *src, cplx<T> *dst, const
     constexpr int cnt = LAST ? TP0 : TP0 + s2 - 1;
     const int items = (LAST ? npos : cnt) * Lt * CW;
     const T f = (T)P.scale;
+    // When the CTA size is a multiple of CW x Lt, every item a thread takes has the same j,
+    // so its six twiddles are read once per pass: per item, they were smem reads at a
+    // stride of 2^(m0-1-t) entries — all in one bank, up to 8-way conflicts (ncu,
+    // 1024 x 8: 40 % of shared-memory wavefronts were conflicts)
+    constexpr bool HOIST = KC_THREADS % (CW * Lt) == 0;
+    C w[6];
+    auto twiddles = [&](int j) {
+        w[0] = kc_tw<M0>(stw, t + 1, j);
+        w[1] = kc_tw<M0>(stw, t + 1, j + Lt);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) w[2 + u] = kc_tw<M0>(stw, t + 2, j + u * Lt);
+    };
+    if constexpr (HOIST) twiddles((threadIdx.x / CW) % Lt);
     for (int it = threadIdx.x; it < items; it += KC_THREADS) {
         const int col = it % CW, q = it / CW, j = q % Lt, p = q / Lt;
         const C a0 = src[(p * Lt + j) * CW + col], a1 = src[((p + s2) * Lt + j) * CW + col];
         const C a2 = src[((p + 2 * s2) * Lt + j) * CW + col];
         const C a3 = src[((p + 3 * s2) * Lt + j) * CW + col];
-        const C w1a = stw[j << (M0 - 1 - t)], w1b = stw[(j + Lt) << (M0 - 1 - t)];
-        const C b0 = bfly<EXACT>(a0, w1a, a2), b1 = bfly<EXACT>(a0, w1b, a2);  // level t+1 at p
-        const C c0v = bfly<EXACT>(a1, w1a, a3), c1 = bfly<EXACT>(a1, w1b, a3);  // at p + s_{t+2}
+        if constexpr (!HOIST) twiddles(j);
+        const C b0 = bfly<EXACT>(a0, w[0], a2), b1 = bfly<EXACT>(a0, w[1], a2);  // level t+1 at p
+        const C c0v = bfly<EXACT>(a1, w[0], a3), c1 = bfly<EXACT>(a1, w[1], a3);  // at p + s_{t+2}
         C o[4];
-        o[0] = bfly<EXACT>(b0, stw[j << (M0 - 2 - t)], c0v);
-        o[1] = bfly<EXACT>(b1, stw[(j + Lt) << (M0 - 2 - t)], c1);
-        o[2] = bfly<EXACT>(b0, stw[(j + 2 * Lt) << (M0 - 2 - t)], c0v);
-        o[3] = bfly<EXACT>(b1, stw[(j + 3 * Lt) << (M0 - 2 - t)], c1);
+        o[0] = bfly<EXACT>(b0, w[2], c0v);
+        o[1] = bfly<EXACT>(b1, w[3], c1);
+        o[2] = bfly<EXACT>(b0, w[4], c0v);
+        o[3] = bfly<EXACT>(b1, w[5], c1);
         if constexpr (LAST) {
             if (col >= ncol) continue;
             const int64_t cc = c0 + col;
@@ -127,7 +160,7 @@ __device__ __forceinline__ void kc_pass4(const cplx<T> *src, cplx<T> *dst, const
     }
 }
 
-template <typename T, bool EXACT, int M0, int TP0, int CW, bool LAST>
+template <typename T, bool EXACT, int M0, int TP0, int CW, bool LAST, int KC_THREADS>
 __device__ __forceinline__ void kc_pass2(const cplx<T> *src, cplx<T> *dst, const cplx<T> *stw,
                                          int npos, int ncol, const KCParams &P, int64_t r0,
                                          int64_t c0) {
@@ -157,9 +190,11 @@ __device__ __forceinline__ void kc_pass2(const cplx<T> *src, cplx<T> *dst, const
 }
 
 template <typename T, bool EXACT, int M0, bool DEEP>
-__global__ void __launch_bounds__(KC_THREADS) kc_cols_kernel(const __grid_constant__ KCParams P) {
+__global__ void __launch_bounds__(KCShape<T, M0, DEEP>::THREADS)
+    kc_cols_kernel(const __grid_constant__ KCParams P) {
     using C = cplx<T>;
     using S = KCShape<T, M0, DEEP>;
+    constexpr int KC_THREADS = S::THREADS;
     constexpr int n0 = 1 << M0, TP0 = S::TP0, CW = S::CW;
     constexpr int W = TP0 + n0 - 1;
     extern __shared__ __align__(16) unsigned char kc_smem_raw[];
@@ -168,6 +203,10 @@ __global__ void __launch_bounds__(KC_THREADS) kc_cols_kernel(const __grid_consta
     C *stw = bufB + CW * kc_buf(M0, TP0, 1);  // Omega_n0[k] (make_twiddles(1024), stride 1024/n0)
     for (int k = threadIdx.x; k < n0; k += KC_THREADS)
         stw[k] = __ldg(static_cast<const C *>(P.tw) + (k << (10 - M0)));
+    for (int e = threadIdx.x; e < kc_tw_entries(M0) - n0; e += KC_THREADS) {
+        const int l = 31 - __clz(e + 2), k = e + 2 - (1 << l);  // table L = 2^l, entry k
+        stw[n0 + e] = __ldg(static_cast<const C *>(P.tw) + (k << (10 - l)));
+    }
     const C *z = static_cast<const C *>(P.z);
     const int64_t ctiles = (P.cols + CW - 1) / CW;
     const int64_t ntiles = ctiles * ((P.P0s + TP0 - 1) / TP0);
@@ -215,12 +254,12 @@ __global__ void __launch_bounds__(KC_THREADS) kc_cols_kernel(const __grid_consta
         }
         __syncthreads();
         if constexpr (M0 == 1) {
-            kc_pass2<T, EXACT, M0, TP0, CW, true>(bufA, nullptr, stw, npos, ncol, P, r0, c0);
+            kc_pass2<T, EXACT, M0, TP0, CW, true, KC_THREADS>(bufA, nullptr, stw, npos, ncol, P, r0, c0);
         } else {
             constexpr int T0 = M0 % 2;
             C *src = bufA, *dst = bufB;
             if constexpr (T0 == 1) {
-                kc_pass2<T, EXACT, M0, TP0, CW, false>(src, dst, stw, npos, ncol, P, r0, c0);
+                kc_pass2<T, EXACT, M0, TP0, CW, false, KC_THREADS>(src, dst, stw, npos, ncol, P, r0, c0);
                 __syncthreads();
                 src = bufB;
                 dst = bufA;
@@ -228,9 +267,9 @@ __global__ void __launch_bounds__(KC_THREADS) kc_cols_kernel(const __grid_consta
             static_for<(M0 - T0) / 2>([&](auto kcc) {
                 constexpr int t = T0 + 2 * decltype(kcc)::value;
                 if constexpr (t + 2 == M0) {
-                    kc_pass4<T, EXACT, M0, TP0, CW, t, true>(src, nullptr, stw, npos, ncol, P, r0, c0);
+                    kc_pass4<T, EXACT, M0, TP0, CW, t, true, KC_THREADS>(src, nullptr, stw, npos, ncol, P, r0, c0);
                 } else {
-                    kc_pass4<T, EXACT, M0, TP0, CW, t, false>(src, dst, stw, npos, ncol, P, r0, c0);
+                    kc_pass4<T, EXACT, M0, TP0, CW, t, false, KC_THREADS>(src, dst, stw, npos, ncol, P, r0, c0);
                     __syncthreads();
                     C *tmp = src;
                     src = dst;
@@ -251,7 +290,7 @@ static int kc_launch_one(const KCParams &P, cudaStream_t st, int64_t *rows_per_s
         return -2;
     if (rows_per_strip_hint) *rows_per_strip_hint = S::TP0;
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, KC_THREADS, S::SMEM) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, S::THREADS, S::SMEM) != cudaSuccess ||
         occ < 1)
         return -2;
     const int64_t tiles = ((P.cols + S::CW - 1) / S::CW) * ((P.P0s + S::TP0 - 1) / S::TP0);
@@ -270,7 +309,7 @@ static int kc_launch_one(const KCParams &P, cudaStream_t st, int64_t *rows_per_s
     // profiles/bench_large_r01b.jsonl, bench_kd_r01b.jsonl.
     const bool oneshot =
         force >= 0 ? force == 1 : (DEEP && M0 >= 4 && M0 < 9 && tiles >= 3 * slots);
-    fn<<<(unsigned)((oneshot || tiles < slots) ? tiles : slots), KC_THREADS, S::SMEM, st>>>(P);
+    fn<<<(unsigned)((oneshot || tiles < slots) ? tiles : slots), S::THREADS, S::SMEM, st>>>(P);
     return 0;
 }
 
