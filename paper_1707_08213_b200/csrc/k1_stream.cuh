@@ -167,24 +167,31 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
     // units — each column block is its n0 - 1 warm-up rows followed by its window rows —
     // so a share that crosses into the next column block pays for that block's warm-up
     // out of its share, and every CTA costs its share plus at most one warm-up of its own
-    const int64_t rows_all = P.p0_end - P.p0_begin;
-    const int64_t U = rows_all + (n0 - 1);
-    int64_t lin = 0, lin_end = 0;
-    if (P.streamk) {
-        const int64_t L = P.CB * U;
-        lin = (int64_t)blockIdx.x * L / gridDim.x;
-        lin_end = (int64_t)(blockIdx.x + 1) * L / gridDim.x;
+    // (kept in shared memory: the share cursor is CTA-uniform, and in registers it cost the
+    // largest fp64 instantiations a spill)
+    __shared__ int64_t s_lin, s_lin_end;
+    if (P.streamk && tid == 0) {
+        const int64_t L = P.CB * (P.p0_end - P.p0_begin + (n0 - 1));
+        s_lin = (int64_t)blockIdx.x * L / gridDim.x;
+        s_lin_end = (int64_t)(blockIdx.x + 1) * L / gridDim.x;
     }
+    __syncthreads();
     for (int64_t tile = blockIdx.x;;) {
         int64_t cb, r0, r1;  // column block, output rows [r0, r1)
         if (P.streamk) {
+            const int64_t lin = s_lin, lin_end = s_lin_end;
             if (lin >= lin_end) break;
+            const int64_t U = P.p0_end - P.p0_begin + (n0 - 1);
             cb = lin / U;
             const int64_t cend = (cb + 1) * U;
             const int64_t se = lin_end < cend ? lin_end : cend;
             const int64_t a = lin - cb * U - (n0 - 1), e = se - cb * U - (n0 - 1);
-            lin = se;
-            if (e <= 0) continue;  // the share ends inside this block's warm-up: no rows
+            __syncthreads();  // every thread has read the cursor
+            if (tid == 0) s_lin = se;
+            if (e <= 0) {  // the share ends inside this block's warm-up: no rows
+                __syncthreads();
+                continue;
+            }
             r0 = P.p0_begin + (a > 0 ? a : 0);
             r1 = P.p0_begin + e;
         } else {
