@@ -461,10 +461,13 @@ struct K1Choice {
 // Q = 2 over 3 (32x16: 574 -> 865 Gcoef/s, 32x32: 552 -> 860, 32x8 / config 3: 808 -> 857);
 // 16x16 runs with a 5-CTA register cap (config 2 0.0902 vs 0.0922 ms, config 4 level).
 // 256-row windows (m0 = 8, fp32 only) take Q = 4 so their register ring stays at 32 complex.
+// 64x64 (config 5) takes Q = 2 (256 threads, 244 registers, one CTA per SM like Q = 3's 512)
+// since the warm-up skip: 19.60 -> 19.09 ms and 20.68 -> 20.08 in two passes
+// (profiles/tune_r02_c5.jsonl; config 5 runs at the 1000 W software power cap).
 constexpr K1Choice K1_TUNED_FP32[] = {
     {2, 2, 1, 8},  {2, 3, 0, 32}, {3, 2, 2, 8}, {3, 4, 1, 4}, {4, 2, 2, 16}, {4, 3, 2, 8},
     {4, 4, 2, 2, 5}, {4, 6, 1, 1}, {5, 2, 3, 8}, {5, 3, 2, 4}, {5, 4, 2, 2},  {5, 5, 2, 1},
-    {5, 6, 2, 1},  {6, 2, 3, 2},  {6, 3, 3, 2}, {6, 4, 3, 1}, {6, 5, 3, 1},
+    {5, 6, 2, 1},  {6, 2, 3, 2},  {6, 3, 3, 2}, {6, 4, 3, 1}, {6, 5, 3, 1}, {6, 6, 2, 1},
     {8, 0, 4, 8},  {8, 1, 4, 4},  {8, 2, 4, 2},  {9, 0, 5, 4},  {9, 1, 5, 2},
 };
 // fp64 (exact) from the fp64 window sweep (profiles/sweep64_r01c.jsonl): the rule's

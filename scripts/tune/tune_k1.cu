@@ -28,8 +28,9 @@ struct Variant { const char *name; const K1Info *(*info)(); };
     {"double m0=" #M0 " m1=" #M1 " Q=" #Q " TP1=" #TP1 " MINB=" #MINB,                  \
      &k1_info<double, M0, M1, Q, TP1, true, MINB, 1>}
 static const Variant VARIANTS[] = {
-    // tall windows: 1024 x 8 / 1024 x 1 (Q = 6), 512 x 8 (Q = 5)
-    V(float, 10, 3, 6, 1, 1, 1), V(float, 10, 0, 6, 8, 1, 1), V(float, 9, 3, 5, 1, 1, 1),
+    // 64x64 (c5): residue groups / CTA width under the power cap
+    V(float, 6, 6, 3, 1, 1, 1), V(float, 6, 6, 2, 1, 1, 1), V(float, 6, 6, 2, 2, 1, 1),
+    V(float, 6, 6, 4, 1, 1, 1), V(float, 6, 6, 2, 1, 2, 1),
 };
 }  // namespace swdft2d
 
