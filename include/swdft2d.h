@@ -139,12 +139,16 @@ int swdft2d_workspace_bytes(int64_t N0, int64_t N1, int m0, int m1, int prec, in
  * The K1 launch schedule swdft2d_forward would use for window rows [p0_begin, p0_end)
  * on the current device (for tests and tuning; the reference has no equivalent):
  *   info = {mode (0 uniform row chunks on a persistent grid, 1 guided big-first chunks
- *           on a persistent grid with a tile counter, 2 one-shot grid: one CTA per tile),
+ *           on a persistent grid with a tile counter, 2 one-shot grid: one CTA per tile,
+ *           3 stream-K: grid CTAs each take an equal contiguous share of the
+ *           column-block-major (column block, window row) space in cost units — every
+ *           column block counted as its n0 - 1 warm-up rows plus its window rows — and
+ *           walk it as one tile per column block touched; chunks = 0, no bounds),
  *           rows per tile (uniform), row chunks, tiles, grid CTAs, column blocks,
  *           CTA slots (SMs x occupancy), CTAs per SM}
  *   bounds[c] (c <= chunks, up to max_bounds entries): first window row of chunk c,
  *           relative to p0_begin; bounds[chunks] = p0_end - p0_begin.
- * Honours the SWDFT2D_K1_GUIDED / _ONESHOT / _RCH overrides like the forward call.
+ * Honours the SWDFT2D_K1_GUIDED / _ONESHOT / _RCH / _STREAMK overrides like the forward call.
  * SWDFT2D_E_UNSUPPORTED if (m0, m1, prec) has no K1 instantiation.
  */
 int swdft2d_k1_schedule(int64_t N0, int64_t N1, int m0, int m1, int prec, int64_t p0_begin,

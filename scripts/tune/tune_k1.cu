@@ -28,9 +28,10 @@ struct Variant { const char *name; const K1Info *(*info)(); };
     {"double m0=" #M0 " m1=" #M1 " Q=" #Q " TP1=" #TP1 " MINB=" #MINB,                  \
      &k1_info<double, M0, M1, Q, TP1, true, MINB, 1>}
 static const Variant VARIANTS[] = {
-    // 64x64 (c5): residue groups / CTA width under the power cap
-    V(float, 6, 6, 3, 1, 1, 1), V(float, 6, 6, 2, 1, 1, 1), V(float, 6, 6, 2, 2, 1, 1),
-    V(float, 6, 6, 4, 1, 1, 1), V(float, 6, 6, 2, 1, 2, 1),
+    // 32x8 (c3): residue groups, CTA width, register cap
+    V(float, 5, 3, 2, 4, 1, 1), V(float, 5, 3, 2, 4, 2, 1), V(float, 5, 3, 2, 4, 3, 1),
+    V(float, 5, 3, 2, 8, 1, 1), V(float, 5, 3, 2, 2, 1, 1), V(float, 5, 3, 3, 2, 1, 1),
+    V(float, 5, 3, 1, 8, 1, 1), V(float, 5, 3, 3, 4, 1, 1),
 };
 }  // namespace swdft2d
 
