@@ -583,3 +583,69 @@ def test_first_call_inside_graph_capture(cuda):
     r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "first_capture_check.py")],
                        capture_output=True, text=True, timeout=300, cwd=ROOT)
     assert "first-call capture ok True" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("split,rank,pieces", [((2, 2), 3, 2), ((4, 1), 2, 3), ((1, 3), 1, 2)])
+def test_pipelined_block_receive_on_device(cuda, monkeypatch, split, rank, pieces):
+    """The receiver side of partition.pipelined_block_forward on the GPU, with the NCCL
+    point-to-point layer replaced by copies on a 'link' stream that deliver each piece
+    late (a device sleep first): the pieces' K1 launches alternate between the current
+    stream and the side stream, each waits for its own piece only, and the rank's block
+    equals its block of the single-device output bitwise (fp64)."""
+    from paper_1707_08213_b200 import partition
+
+    rng = np.random.default_rng(rank)
+    x = torch.from_numpy(rng.standard_normal((90, 77))).to(cuda)
+    m0, m1 = 3, 2
+    n0, n1 = 8, 4
+    P0, P1 = 90 - 7, 77 - 3
+    full = torch.empty((P0, P1, n0, n1), dtype=torch.complex128, device=cuda)
+    forward_into(x, m0, m1, full, prec=_lib.PREC_FP64)
+    a, b, c0, c1, rb, re, cb, ce = partition.block_plan(P0, P1, m0, m1, *split)[rank]
+    link = torch.cuda.Stream(cuda)
+    sent = x[rb:re, cb:ce].contiguous()
+
+    class Op:
+        def __init__(self, fn, tensor, peer, group=None):
+            self.fn, self.tensor, self.peer = fn, tensor, peer
+
+    class Work:
+        def __init__(self, ev):
+            self.ev = ev
+
+        def wait(self):
+            torch.cuda.current_stream(cuda).wait_event(self.ev)
+
+    def fake_batch(ops):
+        works = []
+        for op in ops:
+            assert op.fn is partition.dist.irecv and op.peer == 0
+            row0 = (op.tensor.data_ptr() - local_base[0]) // (op.tensor.stride(0) * 8)
+            link.wait_stream(torch.cuda.current_stream(cuda))
+            with torch.cuda.stream(link):
+                torch.cuda._sleep(200000)  # the piece arrives late
+                op.tensor.copy_(sent[row0:row0 + op.tensor.shape[0]])
+                ev = torch.cuda.Event()
+                ev.record(link)
+            works.append(Work(ev))
+        return works
+
+    recv = torch.full((re - rb, ce - cb), float("nan"), dtype=torch.float64, device=cuda)
+    local_base = [recv.data_ptr()]
+    monkeypatch.setattr(partition.dist, "get_rank", lambda group=None: rank)
+    monkeypatch.setattr(partition.dist, "get_world_size", lambda group=None: split[0] * split[1])
+    monkeypatch.setattr(partition.dist, "P2POp", Op)
+    monkeypatch.setattr(partition.dist, "batch_isend_irecv", fake_batch)
+    out = torch.full((b - a, c1 - c0, n0, n1), float("nan"), dtype=torch.complex128, device=cuda)
+    streams = set()
+
+    def compute(local, w0, w1):
+        streams.add(torch.cuda.current_stream(cuda).cuda_stream)
+        forward_into(local, m0, m1, out[w0:w1], prec=_lib.PREC_FP64, p0_begin=w0, p0_end=w1)
+
+    partition.pipelined_block_forward(None, (90, 77), m0, m1, split, torch.float64, cuda,
+                                      compute, recv=recv, pieces=pieces)
+    torch.cuda.synchronize()
+    assert len(streams) == (2 if min(pieces, b - a) > 1 else 1)
+    assert torch.equal(out.view(torch.float64), full[a:b, c0:c1].contiguous().view(torch.float64))
