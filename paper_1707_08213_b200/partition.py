@@ -153,7 +153,7 @@ def _block_area(p):
     return max(0, p[1] - p[0]) * max(0, p[3] - p[2])
 
 
-def tune_split(x, m0: int, m1: int, prec: int, world: int, reps: int = 2):
+def tune_split(x, m0: int, m1: int, prec: int, world: int, reps: int = 2, src: int = 0):
     """Measure on x's device which gr x gc partition of ``world`` ranks finishes first.
 
     For every factorisation, K1 transforms the largest block a rank would own (from a
@@ -198,7 +198,7 @@ def tune_split(x, m0: int, m1: int, prec: int, world: int, reps: int = 2):
         t = min(ts_)
         send = first = 0
         for g, p in enumerate(plan):
-            if g == 0 or _block_area(p) == 0:
+            if g == src or _block_area(p) == 0:
                 continue
             rows_in, cols_in = p[5] - p[4], p[7] - p[6]
             send += rows_in * cols_in * esz
@@ -228,7 +228,8 @@ def choose_split(x, shape, m0: int, m1: int, prec: int, world: int, in_bytes: in
     if world == 1:
         res = {"split": (1, 1), "pieces": 1, "table": []}
     else:
-        obj = [tune_split(x, m0, m1, prec, world) if dist.get_rank(group) == src else None]
+        obj = [tune_split(x, m0, m1, prec, world, src=src) if dist.get_rank(group) == src
+               else None]
         dist.broadcast_object_list(obj, src=dist.get_global_rank(group, src) if group else src,
                                    group=group)
         res = obj[0]

@@ -145,7 +145,7 @@ def _worker_blocks(rank, world, port, m0, m1, shape, split, pieces, outdir):
         # through the broadcast and is cached per shape, so a second call sends nothing
         calls = []
 
-        def fake_tune(x, m0_, m1_, prec, w):
+        def fake_tune(x, m0_, m1_, prec, w, src=0):
             calls.append(1)
             return {"split": split, "pieces": pieces, "table": [{"split": split}]}
 
