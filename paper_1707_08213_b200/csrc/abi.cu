@@ -77,7 +77,8 @@ static int fail(int code, const char *fmt, ...) {
 }
 
 // ---- K1 registry ---------------------------------------------------------
-static const K1Info *g_k1[SWDFT2D_K1_MAX_M0 + 1][SWDFT2D_K1_MAX_M + 1][2][2];  // [m0][m1][prec][tma]
+// [m0][m1][prec][variant]: 0 LDG input, 1 TMA input, 2 the Z-column kernel (m1 = 0)
+static const K1Info *g_k1[SWDFT2D_K1_MAX_M0 + 1][SWDFT2D_K1_MAX_M + 1][2][3];
 
 void register_k1(const K1Info *info) { g_k1[info->m0][info->m1][info->prec][info->tma] = info; }
 
@@ -100,7 +101,7 @@ static void ensure_registered() {
 const K1Info *find_k1(int m0, int m1, int prec, int tma) {
     ensure_registered();
     if (m0 < 0 || m1 < 0 || m0 > SWDFT2D_K1_MAX_M0 || m1 > SWDFT2D_K1_MAX_M || prec < 0 ||
-        prec > 1 || tma < 0 || tma > 1)
+        prec > 1 || tma < 0 || tma > 2)
         return nullptr;
     return g_k1[m0][m1][prec][tma];
 }
@@ -316,10 +317,39 @@ static int64_t sep_strip_rows(int64_t zrow, int64_t n0, int64_t rows, int64_t ws
 // swdft2d_workspace_bytes; a smaller one just means shorter strips); without one the
 // library takes <= ~512 MB stream-ordered from the device pool for the call
 // (cudaMallocAsync / cudaFreeAsync on the caller's stream).
+static int run_k1(DeviceState *ds, const K1Info *k1, K1Params &P, const CUtensorMap &tmap,
+                  int64_t p0_begin, int64_t p0_end, const void *tw64, cudaStream_t st);
+// Column trees of the large-window path: K1's 1-column Z-column kernel (n0 x 1 over Z,
+// columns decomposed as (p1, k1), K1Params::col_m1) or KC.  K1 streams down the rows
+// with the tree's reuse along p0 (no halo recompute, no Z re-reads) but pays an n0 - 1
+// row warm-up per tile; KC recomputes each tile's halo.  Measured per window
+// (scripts/sep_cols_sweep.py, ~4 GB outputs, profiles/sep_cols_r02_{kc,k1}.jsonl), K1 / KC:
+// n1 = 128 with n0 = 2..64 1.02-1.22 (fp32 and fp64); 8x1024 1.12; 128x128 1.39 / 1.13
+// (fp32 / fp64); 256x16, 256x64 fp32 1.13; 128x32 fp64 0.81 (the fp64 128-row kernel
+// runs at 252 registers); 512-row fp32 0.91-0.94.  Short strips of small windows lose to
+// K1's per-tile warm-up (8x1024 fp64 on 29 window rows: 0.92; 3-D 16x8x4 on 81: 0.83;
+// 64x1024 on 8: 0.45), while tall windows win even on strips shorter than n0 (256x64 on
+// 175 rows 1.13, 128x128 fp64 on 119 rows 1.13: KC's halo recompute grows with n0).  So K1
+// for fp32 n0 <= 256, fp64 n0 <= 64 (and 128 when n1 >= 64), on strips of >= 32 window
+// rows, and >= 8 n0 rows when n0 <= 16.
+// SWDFT2D_SEP_COLS=kc / k1 forces one (k1 where instantiated).
+static const int g_sep_cols = [] {
+    const char *e = std::getenv("SWDFT2D_SEP_COLS");
+    return e ? (e[0] == 'k' && e[1] == '1' ? 1 : 0) : -1;
+}();
+
+static bool use_k1_columns(int m0, int m_inner, int prec, int64_t rows) {
+    if (g_sep_cols >= 0) return g_sep_cols == 1;
+    const int64_t n0 = (int64_t)1 << m0;
+    if (rows < 32 || (n0 <= 16 && rows < 8 * n0)) return false;
+    if (prec == SWDFT2D_PREC_FP64) return m0 <= 6 || (m0 == 7 && m_inner >= 6);
+    return m0 <= 8;
+}
+
 static int forward_separable(const void *x, int in_dtype, int64_t N1, int64_t ld_x, int m0,
                              int m1, int prec, double scale, int64_t p0_begin, int64_t p0_end,
                              void *out, void *ws, int64_t ws_bytes, cudaStream_t st,
-                             DeviceState *ds, const void *tw) {
+                             DeviceState *ds, const void *tw, const void *tw64) {
     const int64_t n0 = (int64_t)1 << m0, n1 = (int64_t)1 << m1;
     const int64_t P1 = N1 - n1 + 1, cols = P1 * n1;
     const int64_t esz = prec == SWDFT2D_PREC_FP64 ? 16 : 8;
@@ -368,9 +398,29 @@ static int forward_separable(const void *x, int in_dtype, int64_t N1, int64_t ld
         c.out = static_cast<char *>(out) + (a - p0_begin) * P1 * n0 * n1 * esz;
         c.tw = tw;
         c.sms = ds->sms;
-        if (launch_kr(r, m1, prec, st) || launch_kc(c, m0, prec, st))
+        const K1Info *kz = use_k1_columns(m0, m1, prec, b - a) ? find_k1(m0, 0, prec, 2) : nullptr;
+        if (launch_kr(r, m1, prec, st)) {
             rc = fail(SWDFT2D_E_CUDA, "large-window launch setup failed (m0=%d m1=%d)", m0, m1);
-        else if ((ce = cudaGetLastError()) != cudaSuccess)
+        } else if (kz) {
+            K1Params Pz;
+            std::memset(&Pz, 0, sizeof Pz);
+            CUtensorMap tmap;
+            std::memset(&tmap, 0, sizeof tmap);
+            Pz.x = z;
+            Pz.in_dtype = prec == SWDFT2D_PREC_FP64 ? SWDFT2D_IN_C128 : SWDFT2D_IN_C64;
+            Pz.N0 = c.zrows;
+            Pz.N1 = cols;
+            Pz.ldx = cols;
+            Pz.P1 = cols;
+            Pz.out = c.out;
+            Pz.scale = scale;
+            Pz.apply_scale = c.apply_scale;
+            Pz.col_m1 = m1;
+            rc = run_k1(ds, kz, Pz, tmap, 0, b - a, tw64, st);
+        } else if (launch_kc(c, m0, prec, st)) {
+            rc = fail(SWDFT2D_E_CUDA, "large-window launch setup failed (m0=%d m1=%d)", m0, m1);
+        }
+        if (rc == SWDFT2D_OK && (ce = cudaGetLastError()) != cudaSuccess)
             rc = fail(SWDFT2D_E_CUDA, "large-window kernel launch: %s", cudaGetErrorString(ce));
     }
     if (!ws) cudaFreeAsync(z, st);
@@ -565,6 +615,19 @@ static int k1_counter(DeviceState *ds, cudaStream_t s, unsigned long long **out)
     unsigned long long *p = ds->ctr_blocks[used / K1_CTR_BLOCK] + used % K1_CTR_BLOCK;
     ds->ctr[s] = p;
     *out = p;
+    return SWDFT2D_OK;
+}
+
+// Plan and launch K1 over window rows [p0_begin, p0_end) with P's input/output fields set.
+static int run_k1(DeviceState *ds, const K1Info *k1, K1Params &P, const CUtensorMap &tmap,
+                  int64_t p0_begin, int64_t p0_end, const void *tw64, cudaStream_t st) {
+    K1Plan pl;
+    int rc = k1_plan(ds, k1, P.P1, p0_begin, p0_end, &P, &pl);
+    if (rc) return rc;
+    P.tw = static_cast<const double2 *>(tw64);
+    P.counter = nullptr;  // one-shot grids take one tile per CTA: no counter
+    if (pl.guided && !pl.oneshot && (rc = k1_counter(ds, st, &P.counter))) return rc;
+    k1->launch(P, tmap, (int)pl.grid, st);
     return SWDFT2D_OK;
 }
 
@@ -771,7 +834,7 @@ int swdft2d_forward_ws(const void *x, int in_dtype, int64_t N0, int64_t N1, int6
         if (r != 0) return fail(SWDFT2D_E_CUDA, "row-tree kernel launch setup failed (%d)", r);
     } else if (path == PATH_SEP) {
         if ((rc = forward_separable(x, in_dtype, N1, ld_x, m0, m1, prec, scale, p0_begin, p0_end,
-                                    out, workspace, workspace_bytes, st, ds, tw)))
+                                    out, workspace, workspace_bytes, st, ds, tw, tw64)))
             return rc;
     } else if (path == PATH_K1) {
         const K1Info *k1 = find_k1(m0, m1, prec, 0);
@@ -785,8 +848,6 @@ int swdft2d_forward_ws(const void *x, int in_dtype, int64_t N0, int64_t N1, int6
             kernel == SWDFT2D_KERNEL_STREAM_TMA || (kernel == SWDFT2D_KERNEL_AUTO && g_use_tma);
         const K1Info *kt = want_tma ? find_k1(m0, m1, prec, 1) : nullptr;
         if (kt && encode_input_map(kt, x, in_dtype, N0, N1, ld_x, &tmap, &P)) k1 = kt;
-        K1Plan pl;
-        if ((rc = k1_plan(ds, k1, P1, p0_begin, p0_end, &P, &pl))) return rc;
         P.x = x;
         P.in_dtype = in_dtype;
         P.apply_scale = apply ? 1 : 0;
@@ -796,10 +857,7 @@ int swdft2d_forward_ws(const void *x, int in_dtype, int64_t N0, int64_t N1, int6
         P.P1 = P1;
         P.out = out;
         P.scale = scale;
-        P.tw = static_cast<const double2 *>(tw64);
-        P.counter = nullptr;  // one-shot grids take one tile per CTA: no counter
-        if (pl.guided && !pl.oneshot && (rc = k1_counter(ds, st, &P.counter))) return rc;
-        k1->launch(P, tmap, (int)pl.grid, st);
+        if ((rc = run_k1(ds, k1, P, tmap, p0_begin, p0_end, tw64, st))) return rc;
     } else {
         K0Params P;
         std::memset(&P, 0, sizeof P);
@@ -1012,12 +1070,36 @@ int swdft2d_forward_columns(const void *z, int prec, int64_t N0, int64_t cols, i
                     (long long)p0_begin, (long long)p0_end, (long long)P0);
     if (p0_begin == p0_end) return SWDFT2D_OK;
     if (!z || !out) return fail(SWDFT2D_E_INVALID_ARG, "null device pointer");
+    CaptureModeGuard relaxed;
     DeviceState *ds = nullptr;
     int rc = device_state(&ds);
     if (rc) return rc;
     const void *tw64 = nullptr, *tw32 = nullptr;
     if ((rc = k0_tables(ds, &tw64, &tw32))) return rc;
     const int64_t esz = prec == SWDFT2D_PREC_FP64 ? 16 : 8;
+    const cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    // the same choice as forward_separable's column trees (use_k1_columns)
+    const bool want_kz = m_inner < 31 && use_k1_columns(m0, m_inner, prec, p0_end - p0_begin);
+    if (const K1Info *kz = want_kz ? find_k1(m0, 0, prec, 2) : nullptr) {
+        K1Params Pz;
+        std::memset(&Pz, 0, sizeof Pz);
+        CUtensorMap tmap;
+        std::memset(&tmap, 0, sizeof tmap);
+        Pz.x = static_cast<const char *>(z) + p0_begin * ld_z * esz;
+        Pz.in_dtype = prec == SWDFT2D_PREC_FP64 ? SWDFT2D_IN_C128 : SWDFT2D_IN_C64;
+        Pz.N0 = p0_end - p0_begin + n0 - 1;
+        Pz.N1 = cols;
+        Pz.ldx = ld_z;
+        Pz.P1 = cols;
+        Pz.out = out;
+        Pz.scale = scale;
+        Pz.apply_scale = scale == 1.0 ? 0 : 1;
+        Pz.col_m1 = m_inner;
+        if ((rc = run_k1(ds, kz, Pz, tmap, 0, p0_end - p0_begin, tw64, st))) return rc;
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return fail(SWDFT2D_E_CUDA, "column-tree launch: %s", cudaGetErrorString(e));
+        return SWDFT2D_OK;
+    }
     KCParams c;
     std::memset(&c, 0, sizeof c);
     c.z = static_cast<const char *>(z) + p0_begin * ld_z * esz;
@@ -1032,7 +1114,7 @@ int swdft2d_forward_columns(const void *z, int prec, int64_t N0, int64_t cols, i
     c.out = out;
     c.tw = prec == SWDFT2D_PREC_FP64 ? tw64 : tw32;
     c.sms = ds->sms;
-    if (launch_kc(c, m0, prec, reinterpret_cast<cudaStream_t>(stream)))
+    if (launch_kc(c, m0, prec, st))
         return fail(SWDFT2D_E_CUDA, "column-tree launch setup failed (m0=%d)", m0);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return fail(SWDFT2D_E_CUDA, "column-tree launch: %s", cudaGetErrorString(e));

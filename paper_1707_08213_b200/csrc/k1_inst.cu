@@ -20,6 +20,7 @@ template <int M0, int M1> static void reg_pair() {
 // 512-row windows: fp32, n1 <= 2, Q = 5 (a 32-complex register ring again): 512x1 3.7 vs
 // 2.8 TB/s on KR + KC, 512x2 3.9 vs 3.4 (profiles/sweep_m7_r01.jsonl)
 void k1_register_m0_9() {
+    K1ZInst<9, false>::reg();
     K1Inst<9, 0, false>::reg();
     K1Inst<9, 1, false>::reg();
 }
@@ -28,6 +29,7 @@ void k1_register_m0_9() {
 // registers): 256x1 4.4 vs 2.9 TB/s on KR + KC, 256x2 4.8 vs 4.1, 256x4 5.4 vs 5.1
 // (profiles/sweep_m7_r01.jsonl)
 void k1_register_m0_8() {
+    K1ZInst<8, false>::reg();
     K1Inst<8, 0, false>::reg();
     K1Inst<8, 1, false>::reg();
     K1Inst<8, 2, false>::reg();  // (256x8 measured level with KR + KC: 5.25 vs 5.33 TB/s)
@@ -41,6 +43,8 @@ void k1_register_m0_7() {
     // slower on K1 (3.9 / 4.3 / 5.3 vs 4.2 / 5.2 / 5.7)
     K1Inst<7, 0, true>::reg();
     K1Inst<7, 0, false>::reg();
+    K1ZInst<7, true>::reg();
+    K1ZInst<7, false>::reg();
     K1Inst<7, 1, false>::reg();
     K1Inst<7, 2, false>::reg();
     K1Inst<7, 3, false>::reg();
@@ -49,6 +53,10 @@ void k1_register_m0_7() {
 }
 #else
 void SWDFT2D_CAT(k1_register_m0_, K1_M0)() {
+#if K1_M0 > 0
+    K1ZInst<K1_M0, false>::reg();  // the large-window path's column trees
+    K1ZInst<K1_M0, true>::reg();
+#endif
     reg_pair<K1_M0, 0>();
     reg_pair<K1_M0, 1>();
     reg_pair<K1_M0, 2>();

@@ -108,9 +108,10 @@ template <typename C> __device__ __forceinline__ void k1_store(C *p, C v) {
 }
 
 template <typename T, int M0, int M1, int Q, int TP1, bool EXACT, int MINB = 1, int NBM = 1,
-          bool TMA = false>
+          bool TMA = false, bool COLZ = false>
 __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
     k1_stream_kernel(const __grid_constant__ K1Params P, const __grid_constant__ CUtensorMap tmap) {
+    static_assert(!COLZ || (M1 == 0 && !TMA), "the Z-column variant is a 1-column LDG kernel");
     using S = K1Shape<M0, M1, Q, TP1, NBM>;
     using C = cplx<T>;
     constexpr int n0 = S::n0, n1 = S::n1, J = S::J, NB = S::NB, D = S::D;
@@ -152,8 +153,14 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
                     (int)((pbase - tma_shift(pbase)) * P.tma_per_sample), (int)brow);
     };
 
-    // stage C identity: column (pos, k1), output residue j
-    const int k1 = tid % n1, j = (tid / n1) % J, pos = tid / (n1 * J);
+    // stage C identity: column (pos, k1), output residue j.  COLZ (the large-window path's
+    // column trees, abi.cu forward_separable): the 1-column kernel runs over the stage-R
+    // rows Z, whose column c is (p1, k1) = (c >> col_m1, c mod 2^col_m1) of the real
+    // window; consecutive lanes take consecutive columns, i.e. consecutive k1 of the
+    // output [p0][p1][k0][k1] (coalesced stores)
+    const int k1 = tid % n1;
+    const int j = COLZ ? tid / TP1 : (tid / n1) % J;
+    const int pos = COLZ ? tid % TP1 : tid / (n1 * J);
     // stage R identity: lane lam of transform group gam
     const int gam = lane / G, lam = lane % G;
 
@@ -216,6 +223,12 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
         const int64_t ostride = P.P1 * (int64_t)(n0 * n1);
         C *orow = reinterpret_cast<C *>(P.out) + (pbase + pos) * (int64_t)(n0 * n1) + k1 +
                   (r0 - (n0 - 1) - P.p0_begin) * ostride;
+        if constexpr (COLZ) {  // column c = (p1, k1), k0 at stride 2^col_m1; k0 = j first
+            const int64_t c = pbase + pos;
+            orow = reinterpret_cast<C *>(P.out) +
+                   ((((c >> P.col_m1) * n0) + j) << P.col_m1) + (c & ((1LL << P.col_m1) - 1)) +
+                   (r0 - (n0 - 1) - P.p0_begin) * ostride;
+        }
         const int rel_hi = pbase + pos < P.P1 ? (int)(r1 - r0) + n0 - 1 : 0;
 
         // Input samples of this warp's stage-R tasks for one batch, prefetched one
@@ -384,7 +397,26 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
                     });
                     // emit window row p0 = r0 + rel - (n0 - 1); the scale test is a uniform
                     // branch (predicated multiplies would cost issue slots on every row)
-                    if (rel >= n0 - 1 && rel < rel_hi) {
+                    if (COLZ && rel >= n0 - 1 && rel < rel_hi) {
+                        // outputs k0 = j + J u at stride J 2^col_m1: a bumped pointer
+                        // (a runtime stride per u would hold OUTS 64-bit addresses)
+                        const int64_t ustep = (int64_t)J << P.col_m1;
+                        C *o = orow;
+                        if (P.apply_scale) {
+                            const T f = (T)P.scale;
+                            static_for<S::OUTS>([&](auto uc) {
+                                constexpr int u = decltype(uc)::value;
+                                k1_store(o, cscale(cur[u], f));
+                                o += ustep;
+                            });
+                        } else {
+                            static_for<S::OUTS>([&](auto uc) {
+                                constexpr int u = decltype(uc)::value;
+                                k1_store(o, cur[u]);
+                                o += ustep;
+                            });
+                        }
+                    } else if (!COLZ && rel >= n0 - 1 && rel < rel_hi) {
                         if (P.apply_scale) {
                             const T f = (T)P.scale;
                             static_for<S::OUTS>([&](auto uc) {
@@ -423,24 +455,26 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
 
 // Per-instantiation launcher + registry entry.
 template <typename T, int M0, int M1, int Q, int TP1, bool EXACT, int MINB = 1, int NBM = 1,
-          bool TMA = false>
+          bool TMA = false, bool COLZ = false>
 int k1_launch(const K1Params &P, const CUtensorMap &tmap, int grid, cudaStream_t stream) {
     using S = K1Shape<M0, M1, Q, TP1, NBM>;
     constexpr size_t smem = k1_smem_bytes<T, M0, M1, Q, TP1, NBM, TMA>();
-    k1_stream_kernel<T, M0, M1, Q, TP1, EXACT, MINB, NBM, TMA><<<grid, S::NT, smem, stream>>>(P, tmap);
+    k1_stream_kernel<T, M0, M1, Q, TP1, EXACT, MINB, NBM, TMA, COLZ>
+        <<<grid, S::NT, smem, stream>>>(P, tmap);
     return 0;
 }
 
 // Registry entry for an explicit shape (used by K1Inst and by the tuning harness).
+// Variant index: 0 LDG input, 1 TMA input, 2 the Z-column kernel (COLZ).
 template <typename T, int M0, int M1, int Q, int TP1, bool EXACT, int MINB = 1, int NBM = 1,
-          bool TMA = false>
+          bool TMA = false, bool COLZ = false>
 const K1Info *k1_info() {
     using S = K1Shape<M0, M1, Q, TP1, NBM>;
     static const K1Info info = {
-        M0, M1, EXACT ? 1 : 0, Q, TP1, S::NT, S::NB, TMA ? 1 : 0,
+        M0, M1, EXACT ? 1 : 0, Q, TP1, S::NT, S::NB, COLZ ? 2 : TMA ? 1 : 0,
         k1_smem_bytes<T, M0, M1, Q, TP1, NBM, TMA>(),
-        (const void *)&k1_stream_kernel<T, M0, M1, Q, TP1, EXACT, MINB, NBM, TMA>,
-        &k1_launch<T, M0, M1, Q, TP1, EXACT, MINB, NBM, TMA>};
+        (const void *)&k1_stream_kernel<T, M0, M1, Q, TP1, EXACT, MINB, NBM, TMA, COLZ>,
+        &k1_launch<T, M0, M1, Q, TP1, EXACT, MINB, NBM, TMA, COLZ>};
     return &info;
 }
 
@@ -505,6 +539,16 @@ constexpr int k1_choose_minb(int M0, int M1, bool DBL = false) {
         if (DBL && c.m0 == M0 && c.m1 == M1) return c.minb;
     return 1;
 }
+
+// The Z-column kernel of the large-window path (1-column window n0 x 1 over the
+// stage-R rows; COLZ): the 1-column shape's Q, and 256 / J (<= 32) columns per CTA so that
+// a warp stores runs of consecutive k1 and a CTA stays at <= 256 threads (registers).
+template <int M0, bool DBL> struct K1ZInst {
+    using T = typename std::conditional<DBL, double, float>::type;
+    static constexpr int Q = k1_choose_q(M0, 0, DBL);
+    static constexpr int TP1 = cmin(32, cmax(1, 256 >> Q));
+    static void reg() { register_k1(k1_info<T, M0, 0, Q, TP1, DBL, 1, 1, false, true>()); }
+};
 
 template <int M0, int M1, bool DBL> struct K1Inst {
     using T = typename std::conditional<DBL, double, float>::type;

@@ -45,6 +45,10 @@ struct K1Params {
     // column-block major, is cut into gridDim.x equal contiguous ranges; CTA b walks
     // range b as one tile per column block it touches (each with its own warm-up)
     int streamk;
+    // 1-column windows (M1 = 0 instantiations) over the large-window path's stage-R rows:
+    // column c of x is (p1, k1) = (c >> col_m1, c mod 2^col_m1) of an n1 = 2^col_m1
+    // window, written to out[p0][p1][k0][k1] (0: plain n0 x 1 windows)
+    int col_m1;
     int sample_bytes;    // bytes per input sample (4, 8, 16)
     int tma_per_sample;  // TMA elements per sample (1, or 2 for complex128)
     int tma_row_bytes;   // bytes of one staged input row (TMA box width, 16-B multiple)
