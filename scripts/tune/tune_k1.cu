@@ -27,11 +27,13 @@ struct Variant { const char *name; const K1Info *(*info)(); };
 #define V64(M0, M1, Q, TP1, MINB)                                                       \
     {"double m0=" #M0 " m1=" #M1 " Q=" #Q " TP1=" #TP1 " MINB=" #MINB,                  \
      &k1_info<double, M0, M1, Q, TP1, true, MINB, 1>}
+#define VZ(T, M0, Q, TP1)                                                                \
+    {#T " Z-column m0=" #M0 " Q=" #Q " TP1=" #TP1,                                    \
+     &k1_info<T, M0, 0, Q, TP1, (sizeof(T) == 8), 1, 1, false, true>}
 static const Variant VARIANTS[] = {
-    // 32x8 (c3): residue groups, CTA width, register cap
-    V(float, 5, 3, 2, 4, 1, 1), V(float, 5, 3, 2, 4, 2, 1), V(float, 5, 3, 2, 4, 3, 1),
-    V(float, 5, 3, 2, 8, 1, 1), V(float, 5, 3, 2, 2, 1, 1), V(float, 5, 3, 3, 2, 1, 1),
-    V(float, 5, 3, 1, 8, 1, 1), V(float, 5, 3, 3, 4, 1, 1),
+    // Z-column trees of 1024-row windows (the large-window path; KC serves them today)
+    VZ(float, 10, 6, 4), VZ(float, 10, 7, 2), VZ(float, 10, 6, 2), VZ(double, 10, 7, 2),
+    VZ(double, 10, 6, 2),
 };
 }  // namespace swdft2d
 
