@@ -244,10 +244,16 @@ def test_guided_counter_reuse_and_concurrent_streams(cuda):
     {"SWDFT2D_K1_STREAMK": "1"},
     {"SWDFT2D_K1_STREAMK": "3"},
     {"SWDFT2D_K1_STREAMK": "0"},
-], ids=lambda e: ",".join(f"{k[10:]}={v}" for k, v in e.items()))
+    {"SWDFT2D_K1_STREAMK": "2", "SWDFT2D_TMA": "1"},
+    {"SWDFT2D_K1_GUIDED": "1", "SWDFT2D_TMA": "1"},
+    {"SWDFT2D_SEP_COLS": "k1"},
+    {"SWDFT2D_SEP_COLS": "kc"},
+], ids=lambda e: ",".join(f"{k[8:]}={v}" for k, v in e.items()))
 def test_fuzz_under_schedule_overrides(env):
+    # the column-tree overrides act on the large-window path: full window range there
+    k1_only = [] if "SWDFT2D_SEP_COLS" in env else ["--k1-only"]
     r = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "fuzz_parity.py"),
-                        "--cases", "40", "--seed", "23", "--k1-only"],
+                        "--cases", "40", "--seed", "23"] + k1_only,
                        capture_output=True, text=True, timeout=900, env={**os.environ, **env})
     lines = [line for line in r.stdout.splitlines() if line.startswith("{")]
     assert lines, r.stdout + r.stderr
