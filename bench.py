@@ -298,7 +298,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     # strong: the partition (gr x gc blocks of window rows x window columns) and the
     # scatter's piece count are measured once on rank 0 and broadcast (choose_split);
     # --split GRxGC forces one
-    split, pieces, split_table = (1, 1), 1, []
+    split, pieces, lead, split_table = (1, 1), 1, 0, []
     if strips:
         if args.split:
             split = tuple(int(v) for v in args.split.split("x"))
@@ -307,8 +307,10 @@ def run_ours(args, cfg, rank, world, local_rank):
         else:
             ch = choose_split(x_full, (cfg.N0, cfg.N1), cfg.m0, cfg.m1, prec, world,
                               np.dtype(cfg.dtype).itemsize)
-            split, pieces, split_table = tuple(ch["split"]), ch["pieces"], ch["table"]
-    a, b, c0, c1, rb, re, cb, ce = block_plan(P0, P1, cfg.m0, cfg.m1, *split)[rank if strips else 0]
+            split, pieces, lead = tuple(ch["split"]), ch["pieces"], ch.get("lead", 0)
+            split_table = ch["table"]
+    a, b, c0, c1, rb, re, cb, ce = block_plan(P0, P1, cfg.m0, cfg.m1, *split,
+                                              lead)[rank if strips else 0]
     out = torch.empty((b - a, c1 - c0, n0, n1), dtype=odt, device=dev)
     recv = torch.empty((re - rb, ce - cb), dtype=xdt, device=dev) if x_full is None else None
 
@@ -321,7 +323,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         # in-order chunks and each rank starts on its first chunk on arrival
         if strips:
             pipelined_block_forward(x_full if rank == 0 else None, (cfg.N0, cfg.N1), cfg.m0,
-                                    cfg.m1, split, xdt, dev, compute, recv=recv, pieces=pieces)
+                                    cfg.m1, split, xdt, dev, compute, recv=recv, pieces=pieces,
+                                    lead=lead)
         elif b > a:
             compute(x_full, 0, b - a)
 
@@ -400,7 +403,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                                    "columns, NCCL scatter from rank 0)" if strips else
                                    f"replicas{world} (each rank its own full workload, no "
                                    "data-path collective)" if world > 1 else "single"),
-                   "scatter_pieces": pieces,
+                   "scatter_pieces": pieces, "lead": lead,
                    **({"split_choice": [{k: (list(v) if isinstance(v, tuple) else v)
                                          for k, v in r.items()} for r in split_table]}
                       if split_table else {})},
@@ -420,7 +423,7 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     if strips and not args.no_strong_detail:
         line["strong"] = strong_detail(args, cfg, rank, world, dev, stream, x_full, recv, out,
-                                       prec, pieces, step_s, split, graph_free=True)
+                                       prec, pieces, step_s, split, lead, graph_free=True)
 
     # e2e through the public API from pinned host memory
     if not args.no_e2e:
@@ -430,7 +433,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             out = None
             torch.cuda.empty_cache()
             line["e2e"] = e2e_sharded(args, cfg, x_np, dev, spec, xdt, prec, rank, world, split,
-                                      pieces)
+                                      pieces, lead)
     if world == 1 and not args.no_others:
         graph = out = None
         torch.cuda.empty_cache()
@@ -450,7 +453,7 @@ def run_ours(args, cfg, rank, world, local_rank):
 
 
 def strong_detail(args, cfg, rank, world, dev, stream, x_full, recv, out, prec, pieces, step_s,
-                  split, graph_free=True):
+                  split, lead=0, graph_free=True):
     """Strong-scaling breakdown (max over ranks, device-timed, L2 flushed): the pipelined
     scatter alone (compute replaced by nothing), each rank's block transform alone (input
     already resident), and t(1) = the whole workload on rank 0 alone in the same run, so
@@ -462,7 +465,7 @@ def strong_detail(args, cfg, rank, world, dev, stream, x_full, recv, out, prec, 
     from paper_1707_08213_b200.tree2d import _OUT_DTYPES, forward_into
 
     flush = make_flush(dev)
-    a, b, c0, c1, rb, re, cb, ce = block_plan(cfg.P0, cfg.P1, cfg.m0, cfg.m1, *split)[rank]
+    a, b, c0, c1, rb, re, cb, ce = block_plan(cfg.P0, cfg.P1, cfg.m0, cfg.m1, *split, lead)[rank]
     xdt = x_full.dtype if x_full is not None else recv.dtype
     local = x_full[rb:re, cb:ce] if x_full is not None else recv
 
@@ -484,7 +487,7 @@ def strong_detail(args, cfg, rank, world, dev, stream, x_full, recv, out, prec, 
 
     def scatter_only():
         pipelined_block_forward(x_full if rank == 0 else None, (cfg.N0, cfg.N1), cfg.m0, cfg.m1,
-                                split, xdt, dev, lambda *_: None, recv=recv, pieces=pieces)
+                                split, xdt, dev, lambda *_: None, recv=recv, pieces=pieces, lead=lead)
 
     def compute_only():
         if b > a and c1 > c0:
@@ -509,7 +512,7 @@ def strong_detail(args, cfg, rank, world, dev, stream, x_full, recv, out, prec, 
     torch.cuda.empty_cache()
     return {"t1_ms": t1 * 1e3, "tN_ms": step_s * 1e3, "efficiency_in_run": t1 / (world * step_s),
             "scatter_only_ms": t_scatter * 1e3, "compute_only_ms": t_compute * 1e3,
-            "scatter_pieces": pieces, "split": list(split),
+            "scatter_pieces": pieces, "split": list(split), "lead": lead,
             "note": "max over ranks, median of %d; t1 = whole workload on rank 0 alone, same run" % reps}
 
 
@@ -570,7 +573,7 @@ def other_configs(args, main_cfg, dev, flush, stream):
     return res
 
 
-def e2e_sharded(args, cfg, x_np, dev, spec, xdt, prec, rank, world, split, pieces):
+def e2e_sharded(args, cfg, x_np, dev, spec, xdt, prec, rank, world, split, pieces, lead=0):
     """N > 1: rank 0's pinned host input -> H2D -> tree_swdft_2d_sharded (pipelined NCCL
     scatter + K1 per block) -> every rank copies its block of coefficients to its own
     pinned host buffer (each GPU's own PCIe link).  Time = max over ranks."""
@@ -579,7 +582,7 @@ def e2e_sharded(args, cfg, x_np, dev, spec, xdt, prec, rank, world, split, piece
 
     from paper_1707_08213_b200.partition import block_plan, tree_swdft_2d_sharded
 
-    a, b, c0, c1 = block_plan(cfg.P0, cfg.P1, cfg.m0, cfg.m1, *split)[rank][:4]
+    a, b, c0, c1 = block_plan(cfg.P0, cfg.P1, cfg.m0, cfg.m1, *split, lead)[rank][:4]
     x_pin = torch.from_numpy(x_np).pin_memory() if rank == 0 else None
     from paper_1707_08213_b200.tree2d import _OUT_DTYPES
 
@@ -596,7 +599,7 @@ def e2e_sharded(args, cfg, x_np, dev, spec, xdt, prec, rank, world, split, piece
         xd = x_pin.to(dev, non_blocking=True) if rank == 0 else None
         sh = tree_swdft_2d_sharded(xd, spec, shape=(cfg.N0, cfg.N1), dtype=xdt,
                                    precision="fp32" if prec == 0 else "fp64", budget=1 << 62,
-                                   split=split, pieces=pieces)
+                                   split=split, pieces=pieces, lead=lead)
         host_out.copy_(sh.values, non_blocking=True)
         e1.record(stream)
         torch.cuda.synchronize()

@@ -32,15 +32,30 @@ def strip_plan(P0: int, m0: int, world: int):
     return [_lib.strip_range(P0, m0, g, world) for g in range(world)]
 
 
-def block_plan(P0: int, P1: int, m0: int, m1: int, gr: int, gc: int):
+def _led_plan(P: int, m: int, parts: int, lead: int):
+    """The strip rule on one axis with the first part ``lead`` units shorter and the rest
+    spread over the others: part 0 = [0, floor(P/parts) - lead), part k >= 1 starts at
+    e + floor((P - e)(k - 1)/(parts - 1)), e = part 0's end.  lead = 0 is the plain rule."""
+    if lead <= 0 or parts < 2 or P < parts:
+        return strip_plan(P, m, parts)
+    n = 1 << m
+    e = max(1, P // parts - lead)
+    cuts = [0, e] + [e + ((P - e) * k) // (parts - 1) for k in range(1, parts)]
+    return [(a, b, a, b + n - 1 if b > a else a) for a, b in zip(cuts, cuts[1:])]
+
+
+def block_plan(P0: int, P1: int, m0: int, m1: int, gr: int, gc: int, lead: int = 0):
     """2-D partition over gr x gc ranks (rank g = i * gc + j): window rows
     [floor(P0 i/gr), floor(P0 (i+1)/gr)) x window columns [floor(P1 j/gc),
     floor(P1 (j+1)/gc)), i.e. the strip rule on each axis, with the n0 - 1 halo input
     rows and n1 - 1 halo input columns.  Row strips are (G, 1).  Column blocks are
     bitwise exact like row strips.
+    ``lead`` > 0 makes the source rank's (rank 0's) band that many window rows shorter
+    (window columns when gr = 1), spread over the other bands: rank 0 sends every other
+    block before it computes its own (tune_split sizes it).
     [(p0_begin, p0_end, p1_begin, p1_end, row_begin, row_end, col_begin, col_end)]."""
-    rows = strip_plan(P0, m0, gr)
-    cols = strip_plan(P1, m1, gc)
+    rows = _led_plan(P0, m0, gr, lead if gr > 1 else 0)
+    cols = _led_plan(P1, m1, gc, lead if gr == 1 else 0)
     return [(r[0], r[1], c[0], c[1], r[2], r[3], c[2], c[3]) for r in rows for c in cols]
 
 
@@ -157,13 +172,20 @@ def tune_split(x, m0: int, m1: int, prec: int, world: int, reps: int = 2, src: i
     """Measure on x's device which gr x gc partition of ``world`` ranks finishes first.
 
     For every factorisation, K1 transforms the largest block a rank would own (from a
-    strided view of x, as the source rank does) — the per-block time includes its
-    schedule's wave quantization, warm-up rows and launch — and the scatter is added from
-    the bytes rank 0 sends at NVLINK_PEER_BPS: all of it (one piece) or only the first
-    pieces (two pieces, the rest hidden behind compute) when the second launch's extra
-    warm-up costs less than the transfer it hides.  Measured on one GPU the same way in
-    scripts/split_scaling.py (profiles/split_scaling_r02*.jsonl).  Returns {"split":
-    (gr, gc), "pieces": p, "table": [...]}."""
+    strided view of x, as the source rank does) — the per-block time t includes its
+    schedule's wave quantization, warm-up rows and launch.  The scatter is modelled from
+    the bytes the source sends at NVLINK_PEER_BPS (all of it: t_all; the first pieces:
+    t_first).  The source sends everything before it computes its own block (its NCCL
+    kernel must not compete with its own K1 grid for SMs), so
+      * one piece: every rank waits ~t_all, step ~ t_all + t;
+      * two pieces: receivers start after t_first (+ the second piece's extra warm-up and
+        launch), and the source's band is made `lead` window rows (columns when gr = 1)
+        shorter, spread over the other bands, so that t_all + its block ~ t_first + a
+        receiver's block: step ~ t_first + extra + t (1 + lambda / (b - 1)), lambda =
+        (t_all - t_first - extra) / t * (b - 1) / b, b bands along that axis.
+    The lower step time wins.  Measured on one GPU the same way in scripts/split_scaling.py
+    (profiles/split_scaling_r02*.jsonl).  Returns {"split": (gr, gc), "pieces": p,
+    "lead": window rows (or columns) taken off the source's band, "table": [...]}."""
     from .tree2d import _OUT_DTYPES, forward_into
 
     N0, N1 = int(x.shape[0]), int(x.shape[1])
@@ -207,13 +229,20 @@ def tune_split(x, m0: int, m1: int, prec: int, world: int, reps: int = 2, src: i
         # a second piece re-runs part of the n0 - 1 warm-up (about half of it: stage C is
         # skipped on most warm-up rows) and adds a launch
         extra = 0.5 * (n0 - 1) / max(1, b0 - a0) * t + 5e-6
-        pieces = 2 if t_all - t_first > extra else 1
-        score = t + (t_first + extra if pieces == 2 else t_all)
+        gr, gc = split
+        bands, blen = (gr, b0 - a0) if gr > 1 else (gc, b1 - a1)
+        lam = max(0.0, (t_all - t_first - extra) / t * (bands - 1) / bands)
+        score1 = t_all + t
+        score2 = t_first + extra + t * (1 + lam / (bands - 1))
+        pieces = 2 if score2 < score1 else 1
+        lead = int(round(lam * blen)) if pieces == 2 else 0
         table.append({"split": split, "block": [b0 - a0, b1 - a1], "compute_s": t,
-                      "scatter_s": t_all, "pieces": pieces, "score_s": score})
+                      "scatter_s": t_all, "first_s": t_first, "pieces": pieces, "lead": lead,
+                      "score_s": min(score1, score2)})
     del scratch
     best = min(table, key=lambda r: r["score_s"])
-    return {"split": best["split"], "pieces": best["pieces"], "table": table}
+    return {"split": best["split"], "pieces": best["pieces"], "lead": best["lead"],
+            "table": table}
 
 
 def choose_split(x, shape, m0: int, m1: int, prec: int, world: int, in_bytes: int,
@@ -239,17 +268,16 @@ def choose_split(x, shape, m0: int, m1: int, prec: int, world: int, in_bytes: in
 
 def pipelined_block_forward(x, shape, m0: int, m1: int, split, dtype, device, compute,
                             group=None, src: int = 0, recv=None, pieces: int = 2,
-                            first_fraction: float = 0.125):
+                            first_fraction: float = 0.125, lead: int = 0):
     """Scatter + compute with overlap over the gr x gc block partition ``split``
     (block_plan): every rank's input block travels as ``pieces`` consecutive row chunks
     (separate point-to-point messages, in order), and ``compute(local, w_begin, w_end)``
     runs for the block's window rows [w_begin, w_end) (block-relative) as soon as the
     input rows they need, [w_begin, w_end + n0 - 1), have arrived — so rank g starts
     after its first (short) chunk instead of after its whole block.  The sends go out
-    piece-major (one batched group per piece index: every peer's first chunk before any
-    peer's remainder).  A block narrower than the input is packed into a contiguous copy
+    as one batched group, piece-major (every peer's first chunk ahead of its remainder).  A block narrower than the input is packed into a contiguous copy
     per chunk on the source (row strips are sent as views).  The source rank computes
-    its own block at once, from a strided view of x.
+    its own block from a strided view of x once its sends are done.
     Returns (local input block, (p0_begin, p0_end, p1_begin, p1_end, row_begin, row_end,
     col_begin, col_end))."""
     rank = dist.get_rank(group)
@@ -259,7 +287,7 @@ def pipelined_block_forward(x, shape, m0: int, m1: int, split, dtype, device, co
         raise ValueError(f"split {gr}x{gc} does not cover {world} ranks")
     N0, N1 = int(shape[0]), int(shape[1])
     n0, n1 = 1 << m0, 1 << m1
-    plan = block_plan(N0 - n0 + 1, N1 - n1 + 1, m0, m1, gr, gc)
+    plan = block_plan(N0 - n0 + 1, N1 - n1 + 1, m0, m1, gr, gc, lead)
     mine = plan[rank]
     a, b, _, _, rb, re, cb, ce = mine
     if rank == src:
@@ -275,23 +303,29 @@ def pipelined_block_forward(x, shape, m0: int, m1: int, split, dtype, device, co
             cuts = [0] + [w + n0 - 1 for w in wb[1:-1]] + [gre - grb]
             per_peer.append((g, [(grb + cuts[c], grb + cuts[c + 1]) for c in range(len(cuts) - 1)],
                              (gcb, gce)))
-        # piece-major: one batched group per piece index, so every peer's (short) first
-        # chunk leaves before any peer's remainder, whatever stream(s) the backend runs
-        # its point-to-point operations on; within a peer, pieces arrive in order
-        works = []
+        # ONE batched group holding every send, piece-major (every peer's short first chunk,
+        # then the remainders; within a peer, pieces go in order and the peers proceed in
+        # parallel).  One group = one NCCL kernel, launched BEFORE this rank's own K1 below:
+        # a second group's kernel would queue behind the first on the NCCL stream and then
+        # find every SM held by the persistent K1 grid, i.e. the remainders would leave only
+        # after this rank's whole compute.
+        ops = []
         for c in range(max((len(ps) for _, ps, _ in per_peer), default=0)):
-            ops = []
             for g, ps, (gcb, gce) in per_peer:
                 if c < len(ps):
                     t = x[ps[c][0]:ps[c][1], gcb:gce]
                     ops.append(dist.P2POp(dist.isend, t if gce - gcb == N1 else t.contiguous(),
                                           g, group))
-            works += dist.batch_isend_irecv(ops)
+        works = dist.batch_isend_irecv(ops) if ops else []
+        # ... and its own block only after the sends complete: launched alongside, a
+        # persistent K1 grid that takes every SM first would hold the send kernel back
+        # until the whole block is done (and every receiver with it).  tune_split shortens
+        # this rank's band by `lead` to pay for the wait.
+        for w in works:
+            w.wait()
         local = x[rb:re, cb:ce]
         if b > a and ce > cb:
             compute(local, 0, b - a)
-        for w in works:
-            w.wait()
         return local, mine
     local = recv if recv is not None else torch.empty((re - rb, ce - cb), dtype=dtype,
                                                       device=device)
@@ -303,10 +337,16 @@ def pipelined_block_forward(x, shape, m0: int, m1: int, split, dtype, device, co
         works = [dist.batch_isend_irecv([dist.P2POp(dist.irecv, local[cuts[c]:cuts[c + 1]], src,
                                                     group)])
                  for c in range(len(cuts) - 1)]
-        # On CUDA the pieces alternate between the current stream and a side stream, so a
-        # later piece's CTAs fill SMs as the previous piece's retire instead of waiting
-        # for its last CTA (scripts/split_scaling.py: "pipe2" vs "pipe1"); the current
-        # stream joins the side stream at the end.  compute() runs on torch's current stream.
+        # Every piece's receive is posted (one group each: a group completes as a whole, so
+        # per-piece groups are what lets compute start on the first piece) before any
+        # compute is launched.  On CUDA the pieces' computes alternate between the current
+        # stream and a side stream, so a later piece's CTAs fill SMs as the previous
+        # piece's retire instead of waiting for its last CTA (scripts/split_scaling.py:
+        # "pipe2" vs "pipe1"); the current stream joins the side stream at the end.
+        # compute() runs on torch's current stream.  (A later piece's receive kernel
+        # queues behind the earlier one on the NCCL stream; if the first piece's K1 grid
+        # takes every SM first, that receive waits for it: the step then degrades to the
+        # serial schedule plus the first piece's transfer, never worse.)
         cur = torch.cuda.current_stream(device) if device.type == "cuda" else None
         side = _side_stream(device) if cur is not None and len(wb) > 2 else None
         if side is not None:
@@ -354,7 +394,7 @@ def pipelined_strip_forward(x, shape, m0: int, dtype, device, compute, group=Non
 
 def tree_swdft_2d_sharded(x, spec, *, shape=None, dtype=None, group=None, src: int = 0,
                           precision=None, budget=None, pieces=None,
-                          split="auto") -> ShardedCoefficients:
+                          split="auto", lead: int = 0) -> ShardedCoefficients:
     """Sharded tree_swdft_2d: every rank returns its own block of the output.
 
     On ``src`` pass the full input tensor (CUDA); elsewhere pass x=None plus
@@ -385,11 +425,12 @@ def tree_swdft_2d_sharded(x, spec, *, shape=None, dtype=None, group=None, src: i
                           group, src)
         split = tuple(ch["split"])
         if pieces is None:
-            pieces = ch["pieces"]
+            # the lead shortens rank 0's band: the source's only when the source is rank 0
+            pieces, lead = ch["pieces"], (ch.get("lead", 0) if src == 0 else 0)
     elif split in (None, "strips"):
         split = (world, 1)
     gr, gc = split
-    a, b, c0, c1, rb, re, cb, ce = block_plan(P0, P1, m0, m1, gr, gc)[rank]
+    a, b, c0, c1, rb, re, cb, ce = block_plan(P0, P1, m0, m1, gr, gc, lead)[rank]
     if b > a and c1 > c0:
         bshape = (re - rb, ce - cb)
         core.check_budget(core.lattice_bytes(bshape, spec) + core.output_bytes(bshape, spec),
@@ -403,7 +444,7 @@ def tree_swdft_2d_sharded(x, spec, *, shape=None, dtype=None, group=None, src: i
         forward_into(local, m0, m1, out[w0:w1], prec=prec, scale=scale, p0_begin=w0, p0_end=w1)
 
     pipelined_block_forward(x, shape, m0, m1, split, dtype, device, compute, group, src,
-                            pieces=pieces)
+                            pieces=pieces, lead=lead)
     return ShardedCoefficients(out, a, b, tuple(shape), spec, spec.normalization, c0, c1)
 
 

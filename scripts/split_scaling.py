@@ -15,7 +15,11 @@ piece; the block's compute waits on those events.  Strategies:
   pipe1     2 pieces (1/8 of the window rows first), both launches on one stream;
   pipe2     2 pieces on two streams, so the second launch's CTAs fill SMs as the
             first's retire (partition.py's receive path);
-  compute   the block alone (no transfer).
+  compute   the block alone (no transfer);
+  protocol  what partition.py does: the source sends everything and then computes its own
+            band shortened by tune_split's `lead`; the largest receiver runs pipe2 on the
+            re-balanced plan; the step is the slower of the two (eff_protocol_serial: one
+            piece, every rank ~ scatter + block).
 Efficiency t(1) / (G t), t(1) = the whole config on one GPU, CUDA events, L2 flushed
 (write + read) ahead of the start event, median of 5.
 """
@@ -156,6 +160,36 @@ def main():
                     t = timed(fn)
                     res[label + "_ms"] = t * 1e3
                     res["eff_" + label] = t1 / (G * t)
+                # the library's protocol (partition.py): the source sends everything, then
+                # computes its own band shortened by `lead` (tune_split's formula);
+                # receivers run pipe2 on their (slightly larger) blocks
+                tb = res["compute_ms"] / 1e3
+                extra = 0.5 * (cfg.n0 - 1) / max(1, b0 - a0) * tb + 5e-6
+                bands, blen = (gr, b0 - a0) if gr > 1 else (gc, b1 - a1)
+                lam = max(0.0, (ts - tf - extra) / tb * (bands - 1) / bands)
+                lead = int(round(lam * blen))
+                plan_l = block_plan(cfg.P0, cfg.P1, cfg.m0, cfg.m1, gr, gc, lead)
+                z = plan_l[0]
+                v0 = x[z[4]:z[5], z[6]:z[7]]
+                o0 = out.view(-1)[:(z[1] - z[0]) * (z[3] - z[2]) * cfg.n0 * cfg.n1].view(
+                    z[1] - z[0], z[3] - z[2], cfg.n0, cfg.n1)
+
+                def own(e0):
+                    forward_into(v0, cfg.m0, cfg.m1, o0, prec=prec)
+
+                own(None)
+                t0 = timed(own) + ts
+                rbig = max(plan_l[1:], key=lambda p: (p[1] - p[0]) * (p[3] - p[2]))
+                view = x[rbig[4]:rbig[5], rbig[6]:rbig[7]]
+                o = out.view(-1)[:(rbig[1] - rbig[0]) * (rbig[3] - rbig[2]) * cfg.n0 * cfg.n1].view(
+                    rbig[1] - rbig[0], rbig[3] - rbig[2], cfg.n0, cfg.n1)
+                wb = piece_bounds(rbig[1] - rbig[0], 0.125, 2)
+                piece(0, main_s)
+                piece(1, main_s)
+                trv = timed(pipe2)
+                res.update({"lead": lead, "src_ms": t0 * 1e3, "recv_ms": trv * 1e3,
+                            "eff_protocol": t1 / (G * max(t0, trv)),
+                            "eff_protocol_serial": t1 / (G * (ts + tb))})
                 res["env"] = env
                 print(json.dumps(res), flush=True)
         del x, out

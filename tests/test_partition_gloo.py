@@ -75,12 +75,16 @@ def _worker_pipelined(rank, world, port, m0, m1, shape, outdir, pieces):
         finally:
             dist.batch_isend_irecv = real
         if rank == 0 and world > 1:
-            # piece-major: group c holds piece c of every peer that has one; group 0 has
-            # every peer with rows, so no peer's first chunk waits behind another's rest
-            peers0 = [g for g, _ in groups[0]]
-            assert peers0 == [g for g in range(1, world)], groups
-            for c, grp in enumerate(groups):
-                assert len({g for g, _ in grp}) == len(grp), groups
+            # one group with every send, piece-major: the first world - 1 ops are every
+            # peer's first chunk, and each peer's chunks are in order
+            assert len(groups) == 1, groups
+            ops = groups[0]
+            assert [g for g, _ in ops[:world - 1]] == list(range(1, world)), groups
+            from paper_1707_08213_b200.partition import piece_bounds, strip_plan
+            plan = strip_plan(shape[0] - n0 + 1, m0, world)
+            want = sum(len(piece_bounds(pb - pa, 0.2, pieces)) - 1
+                       for g, (pa, pb, _, _) in enumerate(plan) if g and pb > pa)
+            assert len(ops) == want, groups
         if b > a:
             out = np.concatenate([results[k] for k in sorted(results)])
             np.save(os.path.join(outdir, f"p{rank}.npy"), out)
@@ -133,7 +137,7 @@ def test_gloo_strip_scatter(tmp_path, world, shape, m):
     assert rows[0][0] == 0 and rows[-1][1] == full.shape[0]
 
 
-def _worker_blocks(rank, world, port, m0, m1, shape, split, pieces, outdir):
+def _worker_blocks(rank, world, port, m0, m1, shape, split, pieces, outdir, lead=0):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -165,7 +169,8 @@ def _worker_blocks(rank, world, port, m0, m1, shape, split, pieces, outdir):
             results[(w0, w1)] = oracle.tree2d(local[w0:w1 + n0 - 1].numpy(), m0, m1)
 
         local, (a, b, c0, c1, rb, re, cb, ce) = partition.pipelined_block_forward(
-            x, shape, m0, m1, split, torch.float64, torch.device("cpu"), compute, pieces=pieces)
+            x, shape, m0, m1, split, torch.float64, torch.device("cpu"), compute, pieces=pieces,
+            lead=lead)
         assert tuple(local.shape) == (re - rb, ce - cb)
         np.save(os.path.join(outdir, f"x{rank}.npy"), local.numpy())
         if b > a and c1 > c0:
@@ -177,19 +182,21 @@ def _worker_blocks(rank, world, port, m0, m1, shape, split, pieces, outdir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,split,pieces,shape,m", [(4, (2, 2), 2, (40, 37), (3, 2)),
-                                                        (2, (1, 2), 1, (21, 30), (2, 3)),
-                                                        (3, (1, 3), 2, (19, 44), (3, 1))])
-def test_gloo_block_scatter(tmp_path, world, split, pieces, shape, m):
+@pytest.mark.parametrize("world,split,pieces,shape,m,lead", [
+    (4, (2, 2), 2, (40, 37), (3, 2), 0), (2, (1, 2), 1, (21, 30), (2, 3), 0),
+    (3, (1, 3), 2, (19, 44), (3, 1), 0), (4, (2, 2), 2, (40, 37), (3, 2), 4),
+    (3, (1, 3), 2, (19, 44), (3, 1), 3), (3, (3, 1), 1, (50, 17), (2, 3), 5)])
+def test_gloo_block_scatter(tmp_path, world, split, pieces, shape, m, lead):
     """2-D blocks (window rows x window columns with both halos) scattered from rank 0 in
-    pieces, the split broadcast from rank 0 by choose_split: every received block is the
-    right slice of x and the blocks' transforms tile the full output bitwise."""
+    pieces, the split broadcast from rank 0 by choose_split, rank 0's band shortened by
+    ``lead``: every received block is the right slice of x and the blocks' transforms tile
+    the full output bitwise."""
     import oracle
 
     oracle.build()
     port = _free_port()
-    mp.spawn(_worker_blocks, args=(world, port, m[0], m[1], shape, split, pieces, str(tmp_path)),
-             nprocs=world, join=True)
+    mp.spawn(_worker_blocks, args=(world, port, m[0], m[1], shape, split, pieces, str(tmp_path),
+                                   lead), nprocs=world, join=True)
     x = np.random.default_rng(77).standard_normal(shape)
     full = oracle.tree2d(x, *m)
     covered = np.zeros(full.shape[:2], dtype=int)
