@@ -135,6 +135,7 @@ def main():
         for name, d in per_cfg.items():
             summ.setdefault(name, {}).update(d)
     os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
+    lines += ["", f"Notes on these captures: `ncu_{a.round}_notes.md` (when present)."]
     with open(os.path.join(ROOT, "profiles", f"ncu_{a.round}.md"), "w") as f:
         f.write("\n".join(lines) + "\n")
     with open(summ_path, "w") as f:
