@@ -35,7 +35,7 @@ def main():
     ap.add_argument("--configs", default="c2,c3,c4,c5")
     ap.add_argument("--prec", type=int, default=0, help="0 fp32 / 1 fp64 variants")
     a = ap.parse_args()
-    lib = ctypes.CDLL(os.path.join(HERE, "_build", "libtune.so"))
+    lib = ctypes.CDLL(os.environ.get("TUNE_LIB", os.path.join(HERE, "_build", "libtune.so")))
     lib.tune_name.restype = ctypes.c_char_p
     for name, (res, args) in _lib.SIGNATURES.items():
         getattr(lib, name).restype = res
