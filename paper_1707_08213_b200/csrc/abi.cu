@@ -77,8 +77,9 @@ static int fail(int code, const char *fmt, ...) {
 }
 
 // ---- K1 registry ---------------------------------------------------------
-// [m0][m1][prec][variant]: 0 LDG input, 1 TMA input, 2 the Z-column kernel (m1 = 0)
-static const K1Info *g_k1[SWDFT2D_K1_MAX_M0 + 1][SWDFT2D_K1_MAX_M + 1][2][3];
+// [m0][m1][prec][variant]: 0 LDG input, 1 TMA input, 2 the Z-column kernel (m1 = 0),
+// 3 LDG with float32 input folded at compile time (fp32)
+static const K1Info *g_k1[SWDFT2D_K1_MAX_M0 + 1][SWDFT2D_K1_MAX_M + 1][2][4];
 
 void register_k1(const K1Info *info) { g_k1[info->m0][info->m1][info->prec][info->tma] = info; }
 
@@ -101,7 +102,7 @@ static void ensure_registered() {
 const K1Info *find_k1(int m0, int m1, int prec, int tma) {
     ensure_registered();
     if (m0 < 0 || m1 < 0 || m0 > SWDFT2D_K1_MAX_M0 || m1 > SWDFT2D_K1_MAX_M || prec < 0 ||
-        prec > 1 || tma < 0 || tma > 2)
+        prec > 1 || tma < 0 || tma > 3)
         return nullptr;
     return g_k1[m0][m1][prec][tma];
 }
@@ -848,6 +849,8 @@ int swdft2d_forward_ws(const void *x, int in_dtype, int64_t N0, int64_t N1, int6
             kernel == SWDFT2D_KERNEL_STREAM_TMA || (kernel == SWDFT2D_KERNEL_AUTO && g_use_tma);
         const K1Info *kt = want_tma ? find_k1(m0, m1, prec, 1) : nullptr;
         if (kt && encode_input_map(kt, x, in_dtype, N0, N1, ld_x, &tmap, &P)) k1 = kt;
+        else if (in_dtype == SWDFT2D_IN_F32 && prec == SWDFT2D_PREC_FP32)
+            if (const K1Info *kf = find_k1(m0, m1, prec, 3)) k1 = kf;
         P.x = x;
         P.in_dtype = in_dtype;
         P.apply_scale = apply ? 1 : 0;

@@ -135,6 +135,9 @@ __device__ __forceinline__ double2 load_raw<double>(const void *__restrict__ x, 
 template <>
 __device__ __forceinline__ float2 load_raw<float>(const void *__restrict__ x, int in_dtype,
                                                   int64_t off) {
+#ifdef K1_FORCE_IN_DTYPE  // tuning builds: the input dtype as a compile-time constant
+    in_dtype = K1_FORCE_IN_DTYPE;
+#endif
     switch (in_dtype) {
     case 0: return make_float2(__ldg((const float *)x + off), 0.f);
     case 1: {
@@ -158,6 +161,9 @@ template <> __device__ __forceinline__ double2 from_raw<double>(double2 r, int i
     }
 }
 template <> __device__ __forceinline__ float2 from_raw<float>(float2 r, int in_dtype) {
+#ifdef K1_FORCE_IN_DTYPE
+    in_dtype = K1_FORCE_IN_DTYPE;
+#endif
     if (in_dtype == 1)
         return make_float2((float)__hiloint2double(__float_as_int(r.y), __float_as_int(r.x)), 0.f);
     return r;  // f32 (imaginary +0.0), c64, and c128 (converted at load)

@@ -31,10 +31,8 @@ struct Variant { const char *name; const K1Info *(*info)(); };
     {#T " Z-column m0=" #M0 " Q=" #Q " TP1=" #TP1,                                    \
      &k1_info<T, M0, 0, Q, TP1, (sizeof(T) == 8), 1, 1, false, true>}
 static const Variant VARIANTS[] = {
-    // chain-ring check: 16x16 at 5 and 4 CTAs/SM, 32x8, 64x64 (build with and without
-    // -DK1_NO_CHAIN_RING)
-    V(float, 4, 4, 2, 2, 5, 1), V(float, 4, 4, 2, 2, 4, 1), V(float, 5, 3, 2, 4, 1, 1),
-    V(float, 6, 6, 2, 1, 1, 1),
+    // input-dtype specialisation check (build with and without -DK1_FORCE_IN_DTYPE=0)
+    V(float, 4, 4, 2, 2, 5, 1), V(float, 5, 3, 2, 4, 1, 1),
 };
 }  // namespace swdft2d
 
