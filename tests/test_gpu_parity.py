@@ -461,6 +461,29 @@ def test_row_kernel_windows(cuda, oracle_lib, m1):
     assert bits_equal(run(x, 0, m1, "fp64", normalization="unitary"), refu)
 
 
+@pytest.mark.parametrize("m,rows", [((6, 7), 41), ((3, 7), 80), ((7, 6), 40), ((8, 4), 48),
+                                    ((2, 8), 40)])
+def test_large_windows_column_trees_on_k1(cuda, oracle_lib, m, rows):
+    """Windows of the large-window path with enough window rows that the column trees run
+    on K1's Z-column kernel by the library's rule (abi.cu use_k1_columns): bitwise vs the
+    oracle in fp64 (where the fp64 kernel exists), fp32 in tolerance, and a window-row
+    sub-range (a strip starting mid-array)."""
+    m0, m1 = m
+    n0, n1 = 1 << m0, 1 << m1
+    rng = np.random.default_rng(3 * m0 + m1)
+    N0, N1 = n0 - 1 + rows, n1 + 19
+    x = rng.standard_normal((N0, N1)) + 1j * rng.standard_normal((N0, N1))
+    ref = oracle_lib.tree2d(x, m0, m1, threads=8)
+    got = run(x, m0, m1, "fp64")
+    assert bits_equal(got, ref)
+    assert rel_err(run(x.astype(np.complex64), m0, m1, "fp32"), ref) <= FP32_TOL
+    xt = torch.from_numpy(x).to(cuda)
+    a, b = 3, rows
+    part = torch.empty((b - a, N1 - n1 + 1, n0, n1), dtype=torch.complex128, device=cuda)
+    forward_into(xt, m0, m1, part, prec=_lib.PREC_FP64, p0_begin=a, p0_end=b)
+    assert bits_equal(part.cpu().numpy(), ref[a:b])
+
+
 @pytest.mark.parametrize("m", [(7, 2), (2, 7), (7, 7), (1, 8), (8, 1), (10, 3), (3, 10), (6, 9),
                                (3, 3), (4, 4), (1, 1), (5, 0)])
 def test_separable_large_windows(cuda, oracle_lib, m):
