@@ -542,26 +542,34 @@ static int k1_plan(DeviceState *ds, const K1Info *k1, int64_t P1, int64_t p0_beg
     // Stream-K (equal contiguous shares of the column-block-major row space, one
     // tile per column block a share touches) where the tile grids above quantize badly
     // (profiles/sched_sweep_r02*.jsonl, configs 2-5 and their 2-D partition blocks):
-    //  * uniform chunks: when a k = 1 share is >= 2 warm-ups (n0 - 1 rows), k = share /
-    //    (5 warm-ups) waves of CTAs, clamped to 1..4 (1 when one CTA fills an SM: the SM
-    //    idles between the CTAs of successive waves).  Config 2: 0.0983 -> 0.0932 ms
-    //    (k = 2); column blocks of config 4 (4081 x 511) +7-10 %, config 3 +4-8 %, 32x64 /
-    //    64x32 / 64x64 windows +4-22 %.
-    //  * one-shot grids whose last wave is < 90 % full (column blocks 3.4 x slots:
-    //    +11-13 % on config 5 blocks of 497 columns), k = 1.
+    //  * uniform chunks, when a one-wave share is >= 1 warm-up (n0 - 1 rows);
+    //  * one-shot grids whose last wave is < 90 % full.
+    // In k waves of CTAs: identical shares still finish at very different times (config 2,
+    // one wave: 57-91 us per CTA, scripts/tune/k1_timeline.py), and short CTAs let the
+    // hardware scheduler even that out, until a share is little more than its warm-up:
+    // k = share / (2 warm-ups) in fp32 (3 in fp64), clamped to 1..12 — config 2 k = 2 -> 5:
+    // 0.0908 -> 0.0876-0.0891 ms; column blocks of configs 3-4 k = 8-12 vs 1-4: +2-10 %.
+    // One CTA per SM (64-row windows, 32x64): k = 1 — their SM idles between successive
+    // CTAs (config-5 blocks and 32x64 / 64x64 windows: k = 1 best or within 2 % in 6 of 8
+    // cases, k = 12 up to 9 % slower).  profiles/sched_sweep_r02_waves*.jsonl.
     // Guided schedules stay: long-lived stream-K CTAs spread their stores over the whole
     // output, and on large outputs that measured 3-20 % slower than guided chunks.
     int sk = g_k1_streamk;
     if (sk < 0 && g_k1_oneshot < 0 && g_k1_guided < 0 && !std::getenv("SWDFT2D_K1_RCH")) {
         const int64_t warm = n0 - 1 > 0 ? n0 - 1 : 1;
         const double share = (double)P->CB * (double)rows / (double)slots;
-        sk = 0;
+        bool use = false;
         if (oneshot) {
             const double waves = (double)P->CB / (double)slots;
-            if (waves / std::ceil(waves) < 0.9) sk = 1;
-        } else if (!guided && share >= 2.0 * (double)warm) {
-            const int k = (int)(share / (5.0 * (double)warm));
-            sk = pl->occ == 1 ? 1 : k < 1 ? 1 : k > 4 ? 4 : k;
+            use = waves / std::ceil(waves) < 0.9;
+        } else {
+            use = !guided && share >= (double)warm;
+        }
+        sk = 0;
+        if (use) {
+            const double per = (k1->prec ? 3.0 : 2.0) * (double)warm;
+            const int k = (int)(share / per);
+            sk = pl->occ == 1 ? 1 : k < 1 ? 1 : k > 12 ? 12 : k;
         }
     }
     if (sk > 0) {

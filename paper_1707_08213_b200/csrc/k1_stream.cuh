@@ -55,6 +55,10 @@
 
 namespace swdft2d {
 
+#ifdef K1_TIMELINE  // tuning builds: per-CTA start / end / SM id of the last K1 launch
+__device__ unsigned long long g_k1_timeline[8192][3];
+#endif
+
 __host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
 __host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
 constexpr int pow2ceil(int v) {
@@ -129,6 +133,25 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
     __shared__ __align__(8) uint64_t mbar[S::NSTAGE];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#ifdef K1_TIMELINE
+    if (tid == 0 && blockIdx.x < 8192) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        g_k1_timeline[blockIdx.x][0] = t;
+        g_k1_timeline[blockIdx.x][2] = smid;
+    }
+    struct TimelineEnd {
+        __device__ ~TimelineEnd() {
+            if (threadIdx.x == 0 && blockIdx.x < 8192) {
+                unsigned long long t;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+                g_k1_timeline[blockIdx.x][1] = t;
+            }
+        }
+    } timeline_end;
+#endif
     // input element type: a compile-time constant in the IND >= 0 variants (the per-sample
     // dtype switch folds away), else the launch's
     const int in_dtype = IND >= 0 ? IND : P.in_dtype;

@@ -31,8 +31,7 @@ struct Variant { const char *name; const K1Info *(*info)(); };
     {#T " Z-column m0=" #M0 " Q=" #Q " TP1=" #TP1,                                    \
      &k1_info<T, M0, 0, Q, TP1, (sizeof(T) == 8), 1, 1, false, true>}
 static const Variant VARIANTS[] = {
-    // input-dtype specialisation check (build with and without -DK1_FORCE_IN_DTYPE=0)
-    V(float, 4, 4, 2, 2, 5, 1), V(float, 5, 3, 2, 4, 1, 1),
+    V(float, 4, 4, 2, 2, 5, 1),
 };
 }  // namespace swdft2d
 
@@ -47,3 +46,11 @@ extern "C" int tune_select(int v) {
     swdft2d::register_k1(swdft2d::VARIANTS[v].info());
     return 0;
 }
+
+#ifdef K1_TIMELINE
+// per-CTA (start ns, end ns, smid) of the last K1 launch, n CTAs
+extern "C" int tune_timeline(unsigned long long *dst, int n) {
+    return (int)cudaMemcpyFromSymbol(dst, swdft2d::g_k1_timeline,
+                                     sizeof(unsigned long long) * 3 * (size_t)n);
+}
+#endif
