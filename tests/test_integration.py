@@ -132,3 +132,59 @@ def test_reference_entry_point_device_values(swdft, cuda):
     assert isinstance(dev, core.CoefficientArray) and isinstance(dev.values, torch.Tensor)
     assert dev.values.is_cuda and dev.values.dtype == torch.complex128
     assert np.array_equal(dev.values.cpu().numpy().view(np.uint64), host.values.view(np.uint64))
+
+
+@pytest.mark.gpu
+def test_reference_cli_through_backend(swdft, cuda, tmp_path, capsys):
+    """The reference's own CLI (cli.py:131-185, unmodified) with the backend enabled: its
+    ``transform`` writes a file byte-identical to the one its numpy path writes (window
+    2-D, plain and paper-2d), ``verify`` passes (tree bitwise equal to its swfft_2d, within
+    1e-10 of naive) and fails with --corrupt, and ``bench`` reports the reference's op
+    counts for the tree rows."""
+    import swdft.cli
+
+    import swdft_b200
+
+    x = np.random.default_rng(11).standard_normal((24, 30))
+    src = tmp_path / "x.csv"
+    np.savetxt(src, x, delimiter=",", fmt="%.17g")
+    for window, mode in (("8x4", "none"), ("4x16", "paper-2d")):
+        outs = {}
+        for backend in ("b200", "numpy"):
+            if backend == "numpy":
+                swdft_b200.disable()
+            try:
+                o = tmp_path / f"{backend}_{window}_{mode}.swdf"
+                assert swdft.cli.main(["transform", "--input", str(src), "--output", str(o),
+                                       "--window", window, "--normalization", mode]) == 0
+                outs[backend] = o.read_bytes()
+            finally:
+                swdft_b200.enable()
+        assert outs["b200"] == outs["numpy"]
+    assert swdft.cli.main(["verify", "--input", str(src), "--window", "8x8"]) == 0
+    assert "exact_fft_match=true" in capsys.readouterr().out
+    assert swdft.cli.main(["verify", "--input", str(src), "--window", "8x8", "--corrupt"]) == 1
+    csv = tmp_path / "bench.csv"
+    served = swdft.tree2d.tree_swdft_2d
+    calls = []
+
+    def counting(*a, **k):
+        calls.append(a[0].shape)
+        return served(*a, **k)
+
+    swdft.tree2d.tree_swdft_2d = counting
+    try:
+        assert swdft.cli.main(["bench", "--size", "40x40", "--windows", "4x4,8x2",
+                               "--algorithms", "tree", "--repetitions", "1",
+                               "--output", str(csv)]) == 0
+    finally:
+        swdft.tree2d.tree_swdft_2d = served
+    assert calls and all(c == (40, 40) for c in calls)  # the bench timed the backend
+    lines = csv.read_text().strip().splitlines()
+    head = lines[0].split(",")
+    rows = [dict(zip(head, ln.split(","))) for ln in lines[1:]]
+    assert len(rows) == 2
+    for r in rows:
+        assert r["algorithm"] == "tree"
+        sizes = (int(r["n0"]), int(r["n1"]))
+        assert int(r["ops"]) == swdft.bench.predict_ops("tree", (40, 40), sizes)
