@@ -1,4 +1,5 @@
 """Reference-side binding: the reference package's own ``swdft.tree2d.tree_swdft_2d``
+(and its 1D / kD siblings ``swdft.tree1d.tree_swdft_1d``, ``swdft.treekd.tree_swdft_kd``)
 served by libswdft2d.so on a B200.
 
 This is the module a ``swdft`` maintainer would add: it keeps the
@@ -32,6 +33,7 @@ cannot be loaded, ``enable()`` raises ImportError.
 from __future__ import annotations
 
 import functools
+import importlib
 import os
 import sys
 
@@ -90,8 +92,55 @@ def tree_swdft_2d_b200(x, spec, loop_order: str = "levels-outer", counter=None,
     return core.CoefficientArray(values, x.shape, spec, spec.normalization)
 
 
+def _host_or_device(values):
+    return values if _STATE["values"] == "device" else values.cpu().numpy()
+
+
+def tree_swdft_1d_b200(x, spec, counter=None):
+    """swdft.tree1d.tree_swdft_1d (tree1d.py:29-60) with the compute on the B200 (the 1D
+    tree is the m0 = 0 case of the 2D kernels; bitwise in fp64)."""
+    import numpy as np
+    from swdft import core
+
+    from paper_1707_08213_b200 import tree1d as b200_1d
+
+    x = np.asarray(x, dtype=np.complex128)  # tree1d.py:36-39, the reference's own checks
+    if x.ndim != 1 or spec.k != 1:
+        raise core.ShapeError("tree_swdft_1d expects a 1D signal and 1D window")
+    spec.check_fits(x.shape)
+    r = b200_1d.tree_swdft_1d(x, spec, counter, precision=_STATE["precision"],
+                              device=_STATE["device"])
+    return core.CoefficientArray(_host_or_device(r.values), x.shape, spec, spec.normalization)
+
+
+def tree_swdft_kd_b200(x, spec, counter=None, budget=None):
+    """swdft.treekd.tree_swdft_kd (treekd.py:102-121) with the compute on the B200."""
+    import numpy as np
+    from swdft import core
+
+    from paper_1707_08213_b200 import treekd as b200_kd
+
+    x = np.asarray(x, dtype=np.complex128)  # treekd.py:109-116, the reference's own checks
+    if x.ndim != spec.k:
+        raise core.ShapeError(
+            f"{spec.k}-dimensional window applied to {x.ndim}-dimensional array")
+    spec.check_fits(x.shape)
+    required = core.lattice_bytes(x.shape, spec) + core.output_bytes(x.shape, spec)
+    core.check_budget(required, budget, what="level buffers + coefficient output")
+    r = b200_kd.tree_swdft_kd(x, spec, counter, budget=1 << 62, precision=_STATE["precision"],
+                              device=_STATE["device"])
+    return core.CoefficientArray(_host_or_device(r.values), x.shape, spec, spec.normalization)
+
+
+# (module, attribute, B200 function) the binding routes
+_ROUTES = (("tree2d", "tree_swdft_2d", tree_swdft_2d_b200),
+           ("tree1d", "tree_swdft_1d", tree_swdft_1d_b200),
+           ("treekd", "tree_swdft_kd", tree_swdft_kd_b200))
+
+
 def enable(values: str = "numpy", precision: str = "fp64", device=None) -> None:
-    """Route swdft.tree2d.tree_swdft_2d to libswdft2d.so (idempotent).
+    """Route swdft.tree2d.tree_swdft_2d, swdft.tree1d.tree_swdft_1d and
+    swdft.treekd.tree_swdft_kd to libswdft2d.so (idempotent).
 
     values     "numpy" (the reference's return type) or "device" (a CUDA tensor)
     precision  "fp64" (complex128, bitwise equal to the reference) or "fp32"
@@ -109,16 +158,25 @@ def enable(values: str = "numpy", precision: str = "fp64", device=None) -> None:
     _STATE.update(values=values, precision=precision, device=device)
     if _STATE["orig"] is None:
         _STATE["orig"] = tree2d.tree_swdft_2d
-        tree2d.tree_swdft_2d = functools.wraps(_STATE["orig"])(tree_swdft_2d_b200)
+        _STATE["origs"] = {}
+        for modname, attr, fn in _ROUTES:
+            mod = importlib.import_module("swdft." + modname)
+            orig = getattr(mod, attr)
+            _STATE["origs"][(modname, attr)] = orig
+            setattr(mod, attr, functools.wraps(orig)(fn))
 
 
 def disable() -> None:
-    """Restore the reference's numpy implementation."""
-    from swdft import tree2d
-
+    """Restore the reference's numpy implementations."""
     if _STATE["orig"] is not None:
-        tree2d.tree_swdft_2d = _STATE["orig"]
+        for (modname, attr), orig in _STATE.pop("origs").items():
+            setattr(importlib.import_module("swdft." + modname), attr, orig)
         _STATE["orig"] = None
+
+
+def original(modname: str, attr: str):
+    """The reference's own implementation behind a routed name (while enabled)."""
+    return _STATE["origs"][(modname, attr)]
 
 
 def enabled() -> bool:

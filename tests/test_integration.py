@@ -188,3 +188,66 @@ def test_reference_cli_through_backend(swdft, cuda, tmp_path, capsys):
         assert r["algorithm"] == "tree"
         sizes = (int(r["n0"]), int(r["n1"]))
         assert int(r["ops"]) == swdft.bench.predict_ops("tree", (40, 40), sizes)
+
+
+@pytest.mark.gpu
+def test_reference_1d_kd_entry_points(swdft, cuda, tmp_path):
+    """swdft.tree1d.tree_swdft_1d and swdft.treekd.tree_swdft_kd routed to the B200: the
+    reference's types, exceptions and counter state, output bits equal to its own numpy
+    code; the reference CLI transforms a 3-D SWDF container byte-identically."""
+    import swdft.cli
+    import swdft.container
+    import swdft.tree1d
+    import swdft.treekd
+
+    import swdft_b200
+
+    core, bench = swdft.core, swdft.bench
+    rng = np.random.default_rng(21)
+    o1 = swdft_b200.original("tree1d", "tree_swdft_1d")
+    okd = swdft_b200.original("treekd", "tree_swdft_kd")
+    for N, n, mode in ((50, 8, "none"), (33, 32, "unitary"), (7, 1, "none")):
+        x = rng.standard_normal(N) + 1j * rng.standard_normal(N)
+        spec = core.WindowSpec((n.bit_length() - 1,), mode)
+        c_ref, c_got = bench.OpCounter((N,)), bench.OpCounter((N,))
+        ref = o1(x, spec, counter=c_ref)
+        got = swdft.tree1d.tree_swdft_1d(x, spec, counter=c_got)
+        assert isinstance(got, core.CoefficientArray) and got.normalization == mode
+        assert np.array_equal(got.values.view(np.uint64), ref.values.view(np.uint64))
+        assert c_got.total == c_ref.total
+        assert np.array_equal(c_got.position_ops, c_ref.position_ops)
+    with pytest.raises(core.ShapeError):
+        swdft.tree1d.tree_swdft_1d(np.zeros((4, 4)), core.WindowSpec((1,)))
+    with pytest.raises(core.WindowTooLargeError):
+        swdft.tree1d.tree_swdft_1d(np.zeros(3), core.WindowSpec((2,)))
+    for shape, exps in (((9, 8, 10), (2, 1, 2)), ((6, 6, 6), (1, 1, 1)), ((12, 10), (2, 3))):
+        x = rng.standard_normal(shape)
+        spec = core.WindowSpec(exps)
+        c_ref, c_got = bench.OpCounter(shape), bench.OpCounter(shape)
+        ref = okd(x, spec, counter=c_ref)
+        got = swdft.treekd.tree_swdft_kd(x, spec, counter=c_got)
+        assert isinstance(got, core.CoefficientArray) and got.values.shape == ref.values.shape
+        assert np.array_equal(got.values.view(np.uint64), ref.values.view(np.uint64))
+        assert c_got.total == c_ref.total
+    with pytest.raises(core.ShapeError):
+        swdft.treekd.tree_swdft_kd(np.zeros((4, 4)), core.WindowSpec((1, 1, 1)))
+    with pytest.raises(core.BudgetError) as e:
+        swdft.treekd.tree_swdft_kd(np.zeros((8, 8, 8)), core.WindowSpec((1, 1, 1)), budget=100)
+    with pytest.raises(core.BudgetError) as e_ref:
+        okd(np.zeros((8, 8, 8)), core.WindowSpec((1, 1, 1)), budget=100)
+    assert str(e.value) == str(e_ref.value)
+    # the reference CLI on a 3-D container: same bytes with and without the backend
+    src = tmp_path / "x3.swdf"
+    swdft.container.write_swdf(src, rng.standard_normal((7, 9, 8)).astype(np.complex128))
+    outs = {}
+    for backend in ("b200", "numpy"):
+        if backend == "numpy":
+            swdft_b200.disable()
+        try:
+            o = tmp_path / f"{backend}.swdf"
+            assert swdft.cli.main(["transform", "--input", str(src), "--output", str(o),
+                                   "--window", "4x2x4", "--normalization", "unitary"]) == 0
+            outs[backend] = o.read_bytes()
+        finally:
+            swdft_b200.enable()
+    assert outs["b200"] == outs["numpy"]
