@@ -571,6 +571,18 @@ static int k1_plan(DeviceState *ds, const K1Info *k1, int64_t P1, int64_t p0_beg
             const int k = (int)(share / per);
             sk = pl->occ == 1 ? 1 : k < 1 ? 1 : k > 12 ? 12 : k;
         }
+        // Short launches (at most 2 n0 window rows: push_rows blocks, the first scatter
+        // piece, host-output strips of large windows): every tile is mostly warm-up, and
+        // guided chunks (>= n0 rows each, every one with its own warm-up) or one CTA per
+        // column block waste the most on it.  One wave of equal contiguous shares is the
+        // fastest or level in every measured case once a share holds >= half a warm-up:
+        // config 3 16/32/64 rows 29.7/42.0/60.4 -> 23.6/31.6/52.1 us, config 4 16/32 rows
+        // 35.9/58.4 -> 33.6/52.1, config 5 16..128 rows -2.5..-4 %, config 2 32 rows
+        // 17.4 -> 15.4; fp64 config 4 16/32 rows -3/-11 %, but config 3 below n0 rows
+        // +4 % (so fp64 needs rows >= n0) (profiles/short_launch_r02.jsonl).
+        if (rows <= 2 * (int64_t)n0 && share >= 0.5 * (double)warm &&
+            (k1->prec == 0 || rows >= n0))
+            sk = 1;
     }
     if (sk > 0) {
         const int64_t L = P->CB * rows;

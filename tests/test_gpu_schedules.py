@@ -112,7 +112,7 @@ def test_config5_oneshot_fp64_bitwise(cuda, oracle_lib):
     cfg = CONFIGS["c5"]
     x = cfg.generate()
     xd = torch.from_numpy(x).to(cuda)
-    a0, a1 = 512, 512 + 96
+    a0, a1 = 512, 512 + 160  # > 2 n0 rows: shorter launches take the short-launch rule
     sched = _lib.k1_schedule(cfg.N0, cfg.N1, cfg.m0, cfg.m1, _lib.PREC_FP64, a0, a1)
     assert sched["mode"] == "oneshot", sched
     assert sched["grid"] == sched["tiles"] == sched["column_blocks"]
@@ -260,3 +260,38 @@ def test_fuzz_under_schedule_overrides(env):
     summary = json.loads(lines[-1])
     assert r.returncode == 0 and summary["fails"] == 0, "\n".join(lines)
     assert summary["cases"] >= 30
+
+
+@pytest.mark.parametrize("case", [("c2", 30, 100), ("c3", 40, 1000), ("c4", 32, 2000),
+                                  ("c5", 100, 700)], ids=lambda c: c[0])
+@pytest.mark.parametrize("precision", ["fp64", "fp32"])
+def test_short_launch_streamk_bitwise(cuda, oracle_lib, case, precision):
+    """Launches of at most 2 n0 window rows take one wave of stream-K shares (abi.cu
+    k1_plan, short-launch rule): every row bitwise against KR + KC (fp64) and the oracle on
+    sub-blocks at both ends and the middle of the range; fp32 bitwise against the
+    production launch of the whole config (K1's fp32 results do not depend on tiling)."""
+    name, rows, a0 = case
+    cfg = CONFIGS[name]
+    x = cfg.generate()
+    xd = torch.from_numpy(x).to(cuda)
+    prec = _lib.PREC_FP64 if precision == "fp64" else _lib.PREC_FP32
+    a1 = a0 + rows
+    sched = _lib.k1_schedule(cfg.N0, cfg.N1, cfg.m0, cfg.m1, prec, a0, a1)
+    assert sched["mode"] == "streamk" and sched["grid"] <= sched["slots"], sched
+    odt = torch.complex128 if precision == "fp64" else torch.complex64
+    out = torch.empty((rows, cfg.P1, cfg.n0, cfg.n1), dtype=odt, device=cuda)
+    forward_into(xd, cfg.m0, cfg.m1, out, prec=prec, p0_begin=a0, p0_end=a1)
+    if precision == "fp64":
+        assert compare_with_separable(xd, cfg, out, prec, p0_begin=a0) == []
+        for r in (a0, a0 + rows // 2, a1 - 2):
+            for c in (0, cfg.P1 // 2, cfg.P1 - 48):
+                sub = x[r:r + 2 + cfg.n0 - 1, c:c + 48 + cfg.n1 - 1]
+                ref = oracle_lib.tree2d(sub, cfg.m0, cfg.m1, threads=8)
+                assert bits_equal_np(out[r - a0:r - a0 + 2, c:c + 48].cpu().numpy(), ref), (r, c)
+    else:
+        full = torch.empty((a1 + 1, cfg.P1, cfg.n0, cfg.n1), dtype=odt, device=cuda)
+        forward_into(xd[:a1 + cfg.n0], cfg.m0, cfg.m1, full, prec=prec)
+        assert bits_equal_dev(out, full[a0:a1])
+        del full
+    del out
+    torch.cuda.empty_cache()
