@@ -548,7 +548,16 @@ def other_configs(args, main_cfg, dev, flush, stream):
         stream.wait_stream(cap)
         g.replay()
         ts = []
-        for _ in range(5):
+        # short steps take more samples: on a fresh box single config-2 samples read 0.099-
+        # 0.115 ms against a 0.086-0.088 median (profiles/c2_timing_r02.jsonl), and a median
+        # of 5 once landed on them
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        g.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        reps = 5 if e0.elapsed_time(e1) > 2.0 else 25
+        for _ in range(reps):
             torch.cuda.synchronize()
             flush_l2(flush)  # ahead of the start event (see run_ours)
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -562,6 +571,7 @@ def other_configs(args, main_cfg, dev, flush, stream):
         traffic = ncu_traffic(c.name, pname)
         res[name] = {"desc": c.desc, "dtype": "f32" if prec == _lib.PREC_FP32 else "f64",
                      "value": c.coefficients / t, "unit": UNIT, "kernel_ms": t * 1e3,
+                     "samples": reps,
                      "hbm_write_gbs": c.coefficients * (16 if pname == "fp64" else 8) / t / 1e9,
                      "roofline": {"bound": "hbm", "achieved": alg / t / 1e9, "peak": peak,
                                   "unit": "GB/s", "frac": alg / t / 1e9 / peak,
