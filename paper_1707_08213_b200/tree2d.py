@@ -58,12 +58,9 @@ def _to_tensor(x):
             a = np.asarray(x, dtype=np.complex128)  # raises like the reference does
         t = torch.from_numpy(np.ascontiguousarray(a)) if a.ndim else torch.as_tensor(a)
     if t.dtype not in _IN_CODES:
-        if t.is_complex():
-            t = t.to(torch.complex128)
-        elif t.dtype in (torch.float16, torch.bfloat16):
-            t = t.to(torch.float32)
-        else:
-            t = t.to(torch.float64)
+        # everything else (ints, bools, half floats, complex32) widens exactly to the
+        # reference's own working type, so the default precision is fp64 (bitwise)
+        t = t.to(torch.complex128 if t.is_complex() else torch.float64)
     return t
 
 

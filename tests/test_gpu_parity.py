@@ -202,6 +202,38 @@ def test_input_dtypes_and_strides(cuda, oracle_lib):
     assert bits_equal(out.cpu().numpy(), ref)
 
 
+def test_input_kinds_widen_like_the_reference(cuda, oracle_lib):
+    """Whatever np.asarray(x, complex128) accepts (tree2d.py:189) is widened exactly and, with
+    the default precision, transformed bitwise: nested lists, bools, small ints, half
+    floats, Fortran order, negative strides, read-only arrays, torch host tensors."""
+    rng = np.random.default_rng(9)
+    xr = rng.standard_normal((21, 19))
+    cases = {
+        "list": xr.tolist(),
+        "bool": rng.random((21, 19)) < 0.5,
+        "int8": rng.integers(-100, 100, (21, 19)).astype(np.int8),
+        "uint16": rng.integers(0, 60000, (21, 19)).astype(np.uint16),
+        "int64": rng.integers(-2**40, 2**40, (21, 19)),
+        "float16": xr.astype(np.float16),
+        "fortran": np.asfortranarray(xr),
+        "reversed": xr[::-1, ::-1],
+        "every-other": rng.standard_normal((42, 38))[::2, ::2],
+        "torch-host-bf16": torch.from_numpy(xr).to(torch.bfloat16),
+        "complex-list": (xr + 1j * xr[::-1]).tolist(),
+    }
+    ro = xr.copy()
+    ro.setflags(write=False)
+    cases["read-only"] = ro
+    for name, x in cases.items():
+        wide = x.to(torch.float64).numpy() if isinstance(x, torch.Tensor) else \
+            np.asarray(x, dtype=np.complex128)
+        res = tree_swdft_2d(x, WindowSpec((2, 3)), budget=1 << 40)
+        assert res.values.dtype == torch.complex128, name
+        assert bits_equal(res.values.cpu().numpy(), oracle_lib.tree2d(wide, 2, 3)), name
+    with pytest.raises((TypeError, ValueError)):
+        tree_swdft_2d([["a", "b"], ["c", "d"]], WindowSpec((1, 1)))
+
+
 def test_row_ranges(cuda, oracle_lib):
     """swdft2d_forward on window-row sub-ranges (the strip boundary) is bitwise exact."""
     rng = np.random.default_rng(9)
