@@ -88,6 +88,21 @@ int main(void) {
         const double rel = err / sqrt(norm);
         if (rel > worst) worst = rel;
     }
+    /* the same transform host to host in one call (no CUDA calls on the caller's side):
+     * malloc'd input and output, equal to the device-buffer result bit for bit */
+    float *out2 = (float *)malloc(sizeof(float) * 2 * nout);
+    rc = swdft2d_forward_host(x, SWDFT2D_IN_F32, N0, N1, N1, m0, m1, SWDFT2D_PREC_FP32, 1.0, 0, P0,
+                              out2, (int64_t)(5 * P1 * n0 * n1 * 8), SWDFT2D_KERNEL_AUTO, NULL);
+    if (rc != SWDFT2D_OK) {
+        fprintf(stderr, "swdft2d_forward_host: %d %s\n", rc, swdft2d_last_error());
+        return 1;
+    }
+    for (size_t i = 0; i < 2 * nout; ++i)
+        if (out2[i] != out[i]) {
+            fprintf(stderr, "forward_host differs from forward at %zu\n", i);
+            return 1;
+        }
+    free(out2);
     printf("forward_c: %lld x %lld windows of %d x %d, max window-relative error %.3e\n",
            (long long)P0, (long long)P1, n0, n1, worst);
     cudaFree(x_d);

@@ -136,6 +136,34 @@ int swdft2d_workspace_bytes(int64_t N0, int64_t N1, int m0, int m1, int prec, in
                             int64_t p0_end, int kernel, int64_t *bytes);
 
 /*
+ * Host-to-host forward: the call a numpy-based caller binds (the reference's
+ * tree_swdft_2d takes and returns host arrays, tree2d.py:189,201-202).  Same arguments
+ * as swdft2d_forward, but
+ *   x         host pointer (pageable or pinned; a device pointer also works), N0 x N1
+ *             elements of in_dtype, row stride ld_x
+ *   out_host  host pointer, (p0_end - p0_begin) x P1 x n0 x n1 complex of prec.  Pinned
+ *             memory (swdft2d_host_alloc, cudaHostAlloc, cudaHostRegister) is copied at
+ *             the PCIe rate while later strips compute; pageable memory works at the
+ *             driver's staged rate
+ *   strip_bytes  device bytes per output strip (0: 512 MiB)
+ * The input rows the window rows need are copied to the device, the output is computed
+ * in strips of window rows into a ring of 4 device strips and copied out on two copy
+ * streams while later strips compute, so the device holds at most 4 strips whatever the
+ * output size (outputs larger than HBM are fine).  Compute is ordered on `stream`; the
+ * call is synchronous: out_host is complete on return.  The device scratch (input rows +
+ * ring) is taken stream-ordered from the device's default pool for the call
+ * (cudaMallocAsync / cudaFreeAsync).
+ */
+int swdft2d_forward_host(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t ld_x, int m0,
+                         int m1, int prec, double scale, int64_t p0_begin, int64_t p0_end,
+                         void *out_host, int64_t strip_bytes, int kernel, void *stream);
+
+/* Pinned (page-locked, portable) host memory for swdft2d_forward_host's buffers; NULL on
+ * failure (swdft2d_last_error).  Free with swdft2d_host_free. */
+void *swdft2d_host_alloc(int64_t bytes);
+int swdft2d_host_free(void *p);
+
+/*
  * The K1 launch schedule swdft2d_forward would use for window rows [p0_begin, p0_end)
  * on the current device (for tests and tuning; the reference has no equivalent):
  *   info = {mode (0 uniform row chunks on a persistent grid, 1 guided big-first chunks

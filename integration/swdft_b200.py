@@ -81,13 +81,24 @@ def tree_swdft_2d_b200(x, spec, loop_order: str = "levels-outer", counter=None,
     prec = _precision_code(_STATE["precision"], torch.complex128)
     dev = _STATE["device"] or torch.device("cuda", torch.cuda.current_device())
     odt = torch.complex128 if prec == _lib.PREC_FP64 else torch.complex64
-    xd = torch.from_numpy(np.ascontiguousarray(x)).to(dev)
-    assert xd.dtype in _IN_CODES
-    out = torch.empty((P0, P1, n0, n1), dtype=odt, device=dev)
-    forward_into(xd, m0, m1, out, prec=prec, scale=float(core.normalization_factor(spec)))
+    scale = float(core.normalization_factor(spec))
+    if _STATE["values"] == "device":
+        xd = torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+        assert xd.dtype in _IN_CODES
+        values = torch.empty((P0, P1, n0, n1), dtype=odt, device=dev)
+        forward_into(xd, m0, m1, values, prec=prec, scale=scale)
+    else:
+        # numpy in, a fresh numpy array out, as the reference returns: ONE C-ABI call
+        # (swdft2d_forward_host); the device holds a ring of strips, never the whole output
+        values = np.empty((P0, P1, n0, n1),
+                          dtype=np.complex128 if prec == _lib.PREC_FP64 else np.complex64)
+        di = torch.device(dev).index
+        di = torch.cuda.current_device() if di is None else di
+        with torch.cuda.device(di):
+            _lib.forward_host(np.ascontiguousarray(x), m0, m1, values, prec=prec, scale=scale,
+                              stream=_lib.raw_stream(di))
     if counter is not None:
         _replay_counter(counter, core, x.shape, spec)
-    values = out if _STATE["values"] == "device" else out.cpu().numpy()
     # normalize() would have produced this record: values scaled, mode recorded
     return core.CoefficientArray(values, x.shape, spec, spec.normalization)
 

@@ -46,6 +46,10 @@ SIGNATURES = {
                                _vp, _int, _vp]),
     "swdft2d_forward_ws": (_int, [_vp, _int, _i64, _i64, _i64, _int, _int, _int, _dbl, _i64,
                                   _i64, _vp, _vp, _i64, _int, _vp]),
+    "swdft2d_forward_host": (_int, [_vp, _int, _i64, _i64, _i64, _int, _int, _int, _dbl, _i64,
+                                    _i64, _vp, _i64, _int, _vp]),
+    "swdft2d_host_alloc": (_vp, [_i64]),
+    "swdft2d_host_free": (_int, [_vp]),
     "swdft2d_workspace_bytes": (_int, [_i64, _i64, _int, _int, _int, _i64, _i64, _int, _pi64]),
     "swdft2d_k1_schedule": (_int, [_i64, _i64, _int, _int, _int, _i64, _i64, _pi64, _pi64,
                                    _int]),
@@ -180,3 +184,55 @@ def raw_stream(device_index: int) -> int:
     if get is not None:
         return get(device_index)
     return torch.cuda.current_stream(device_index).cuda_stream
+
+
+def host_empty(shape, dtype):
+    """numpy array over pinned host memory from swdft2d_host_alloc (freed with the array):
+    the output buffer swdft2d_forward_host fills at the PCIe rate."""
+    import weakref
+
+    import numpy as np
+
+    dtype = np.dtype(dtype)
+    n = int(np.prod(shape, dtype=np.int64)) * dtype.itemsize
+    if n == 0:
+        return np.empty(shape, dtype=dtype)
+    lib = load()
+    ptr = lib.swdft2d_host_alloc(n)
+    if not ptr:
+        raise core.DeviceError(last_error())
+    buf = (ctypes.c_char * n).from_address(ptr)
+    weakref.finalize(buf, lib.swdft2d_host_free, ptr)  # buf lives as long as any view of it
+    return np.frombuffer(buf, dtype=dtype).reshape(shape)
+
+
+NP_IN_CODES = {"float32": IN_F32, "float64": IN_F64, "complex64": IN_C64, "complex128": IN_C128}
+
+
+def forward_host(x, m0: int, m1: int, out, *, prec: int, scale: float = 1.0, p0_begin: int = 0,
+                 p0_end: int | None = None, strip_bytes: int = 0, kernel: int = KERNEL_AUTO,
+                 stream: int | None = None):
+    """swdft2d_forward_host on numpy arrays: ``x`` a 2D float32/float64/complex64/complex128
+    array whose rows are contiguous (any row stride), ``out`` a C-contiguous complex array of
+    (p0_end - p0_begin, P1, n0, n1) of the precision (pinned — host_empty — for the PCIe
+    rate).  Synchronous; ``stream`` (a cudaStream_t as int) orders the compute."""
+    code = NP_IN_CODES.get(x.dtype.name)
+    if code is None or x.ndim != 2:
+        raise ValueError(f"forward_host needs a 2D f32/f64/c64/c128 array, got {x.dtype} {x.shape}")
+    N0, N1 = x.shape
+    ld = x.strides[0] // x.itemsize if N0 > 1 else N1
+    if (N1 > 1 and x.strides[1] != x.itemsize) or \
+            (N0 > 1 and (x.strides[0] % x.itemsize or ld < N1)):
+        raise ValueError("forward_host needs contiguous rows at a row stride >= the width")
+    n0, n1 = 1 << m0, 1 << m1
+    if p0_end is None:
+        p0_end = N0 - n0 + 1
+    want = (p0_end - p0_begin, N1 - n1 + 1, n0, n1)
+    odt = "complex64" if prec == PREC_FP32 else "complex128"
+    if tuple(out.shape) != want or out.dtype.name != odt or not out.flags.c_contiguous or \
+            not out.flags.writeable:
+        raise ValueError(f"out must be a writable C-contiguous {odt} array of shape {want}")
+    check(load().swdft2d_forward_host(x.ctypes.data, code, N0, N1, ld, m0,
+                                      m1, prec, float(scale), p0_begin, p0_end, out.ctypes.data,
+                                      strip_bytes, kernel, stream))
+    return out

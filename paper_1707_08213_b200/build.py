@@ -30,7 +30,8 @@ CFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
 
 def _units():
     units = [("abi.cu", [], "abi.o"), ("k0_window.cu", [], "k0_window.o"), ("k2_push.cu", [], "k2_push.o"),
-             ("kr_rows.cu", [], "kr_rows.o"), ("kc_cols.cu", [], "kc_cols.o")]
+             ("kr_rows.cu", [], "kr_rows.o"), ("kc_cols.cu", [], "kc_cols.o"),
+             ("host_pipe.cu", [], "host_pipe.o")]
     for m0 in range(K1_MAX_M + 4):
         units.append(("k1_inst.cu", [f"-DK1_M0={m0}"], f"k1_m0_{m0}.o"))
     return units

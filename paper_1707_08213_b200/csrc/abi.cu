@@ -76,6 +76,16 @@ static int fail(int code, const char *fmt, ...) {
     return code;
 }
 
+int set_error(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
 // ---- K1 registry ---------------------------------------------------------
 // [m0][m1][prec][variant]: 0 LDG input, 1 TMA input, 2 the Z-column kernel (m1 = 0),
 // 3 LDG with float32 input folded at compile time (fp32)
@@ -1160,6 +1170,7 @@ int swdft2d_shutdown(void) {
         }
     }
     g_dev.clear();
+    release_host_pipe();
     cudaSetDevice(cur);
     return SWDFT2D_OK;
 }

@@ -123,4 +123,9 @@ int launch_k2(const K2Params &P, int m0, int m1, int prec, cudaStream_t stream);
 int launch_ring_store(const void *row, int in_dtype, int64_t N1, void *ring, int prec, int n0,
                       int64_t p0, int sms, cudaStream_t stream);
 
+// Sets the calling thread's swdft2d_last_error message; returns code (abi.cu).
+int set_error(int code, const char *fmt, ...) __attribute__((format(printf, 2, 3)));
+// Frees swdft2d_forward_host's cached device scratch and pinned staging (host_pipe.cu).
+void release_host_pipe();
+
 }  // namespace swdft2d

@@ -23,6 +23,8 @@ Differences a caller can observe, all deliberate:
 """
 from __future__ import annotations
 
+import warnings
+
 import numpy as np
 import torch
 
@@ -56,7 +58,12 @@ def _to_tensor(x):
         a = np.asarray(x)
         if a.dtype.kind not in "biufc":
             a = np.asarray(x, dtype=np.complex128)  # raises like the reference does
-        t = torch.from_numpy(np.ascontiguousarray(a)) if a.ndim else torch.as_tensor(a)
+        if a.ndim:
+            with warnings.catch_warnings():  # read-only arrays: the tensor is only ever read
+                warnings.simplefilter("ignore", UserWarning)
+                t = torch.from_numpy(np.ascontiguousarray(a))
+        else:
+            t = torch.as_tensor(a)
     if t.dtype not in _IN_CODES:
         # everything else (ints, bools, half floats, complex32) widens exactly to the
         # reference's own working type, so the default precision is fp64 (bitwise)
@@ -150,39 +157,25 @@ class _nullctx:
         return False
 
 
-def _forward_to_host(xt, m0, m1, host, prec, scale, kernel, strip_bytes, slots=4, copiers=2):
-    """Out-of-core variant: window rows in strips of ~strip_bytes, computed into a ring of
-    `slots` device buffers and copied to the pinned host array `host` on `copiers` copy
-    streams while the next strips compute.  Device memory: slots * strip_bytes."""
-    dev = xt.device
-    P0, P1, n0, n1 = host.shape
-    row_bytes = P1 * n0 * n1 * host.element_size()
-    rows = max(1, min(P0, strip_bytes // max(1, row_bytes)))
-    ring = [torch.empty((rows, P1, n0, n1), dtype=host.dtype, device=dev)
-            for _ in range(min(slots, -(-P0 // rows)))]
-    comp = torch.cuda.current_stream(dev)
-    copy = [torch.cuda.Stream(dev) for _ in range(copiers)]
-    freed = [None] * len(ring)  # event: the slot's previous strip has left the device
-    for k, a in enumerate(range(0, P0, rows)):
-        b = min(P0, a + rows)
-        slot = k % len(ring)
-        if freed[slot] is not None:
-            comp.wait_event(freed[slot])
-        buf = ring[slot][:b - a]
-        forward_into(xt, m0, m1, buf, prec=prec, scale=scale, p0_begin=a, p0_end=b,
-                     kernel=kernel, stream=comp)
-        done = torch.cuda.Event()
-        done.record(comp)
-        cs = copy[k % copiers]
-        cs.wait_event(done)
-        with torch.cuda.stream(cs):
-            host[a:b].copy_(buf, non_blocking=True)
-        freed[slot] = torch.cuda.Event()
-        freed[slot].record(cs)
-        buf.record_stream(cs)
-    for cs in copy:
-        comp.wait_stream(cs)
-    comp.synchronize()
+def _forward_to_host(xt, m0, m1, host, prec, scale, kernel, strip_bytes, device):
+    """Host output: ONE C-ABI call, swdft2d_forward_host (csrc/host_pipe.cu).  The input
+    (host or device tensor) is copied to the device, window rows are computed in strips of
+    ~strip_bytes into a ring of 4 device strips and copied out while later strips compute:
+    straight into a pinned ``host`` (the PCIe rate), or through the library's pinned staging
+    ring and worker threads into a pageable one (a fresh numpy array).  ``host`` is a torch
+    host tensor or a numpy array of (P0, P1, n0, n1); returns it."""
+    lib = _lib.load()
+    if xt.stride(1) != 1 or (xt.shape[0] > 1 and xt.stride(0) < xt.shape[1]):
+        xt = xt.contiguous()
+    N0, N1 = xt.shape
+    ld = xt.stride(0) if N0 > 1 else N1
+    ptr = host.data_ptr() if isinstance(host, torch.Tensor) else host.ctypes.data
+    dev = device.index if device.index is not None else torch.cuda.current_device()
+    with torch.cuda.device(dev):
+        rc = lib.swdft2d_forward_host(xt.data_ptr(), _IN_CODES[xt.dtype], N0, N1, ld, m0, m1, prec,
+                                      float(scale), 0, N0 - (1 << m0) + 1, ptr, int(strip_bytes),
+                                      _lib.KERNELS[kernel], _lib.raw_stream(dev))
+    _lib.check(rc)
     return host
 
 
@@ -230,26 +223,36 @@ def tree_swdft_2d(x, spec, loop_order: str = "levels-outer", counter=None, budge
         device = xt.device if xt.is_cuda else torch.device("cuda", torch.cuda.current_device())
     device = torch.device(device)
     host_mode = to_host or host_out is not None
-    if not xt.is_cuda or xt.device != device:
-        # asynchronous only in host-output mode, which synchronizes before returning; a
-        # call returning a device tensor must not leave a DMA reading the caller's buffer
-        xt = xt.to(device, non_blocking=host_mode and not xt.is_cuda and xt.is_pinned())
     n0, n1 = 1 << m0, 1 << m1
     P0, P1 = shape[0] - n0 + 1, shape[1] - n1 + 1
     scale = core.normalization_factor(spec)
     if host_mode:
-        # host (numpy) output, as the reference returns: strips computed in a small
-        # device ring and streamed to pinned host memory while the next strips compute
+        # host (numpy) output, as the reference returns: one swdft2d_forward_host call.
+        # Without host_out the result is a fresh numpy array (pageable: pinning 34 GB takes
+        # 14-16 s, filling a fresh pageable array through the staging workers 1.0 s)
         want = (P0, P1, n0, n1)
+        odt = _OUT_DTYPES[prec]
+        np_odt = np.complex64 if prec == _lib.PREC_FP32 else np.complex128
         if host_out is None:
-            host_out = torch.empty(want, dtype=_OUT_DTYPES[prec], pin_memory=True)
-        if tuple(host_out.shape) != want or host_out.dtype != _OUT_DTYPES[prec] or \
-                host_out.is_cuda:
-            raise ValueError(f"host_out must be a host {_OUT_DTYPES[prec]} tensor of shape {want}")
-        _forward_to_host(xt, m0, m1, host_out, prec, scale, kernel, strip_bytes)
+            host_out = np.empty(want, dtype=np_odt)
+        if isinstance(host_out, torch.Tensor):
+            ok = not host_out.is_cuda and host_out.dtype == odt and host_out.is_contiguous()
+        else:
+            ok = isinstance(host_out, np.ndarray) and host_out.dtype == np_odt and \
+                host_out.flags.c_contiguous and host_out.flags.writeable
+        if not ok or tuple(host_out.shape) != want:
+            raise ValueError(f"host_out must be a contiguous host {odt} tensor or numpy array "
+                             f"of shape {want}")
+        if xt.is_cuda and xt.device != device:
+            xt = xt.to(device)
+        _forward_to_host(xt, m0, m1, host_out, prec, scale, kernel, strip_bytes, device)
         if counter is not None:
             replay_counter(counter, shape, spec)
-        return CoefficientArray(host_out.numpy(), shape, spec, spec.normalization)
+        values = host_out.numpy() if isinstance(host_out, torch.Tensor) else host_out
+        return CoefficientArray(values, shape, spec, spec.normalization)
+    if not xt.is_cuda or xt.device != device:
+        # a call returning a device tensor must not leave a DMA reading the caller's buffer
+        xt = xt.to(device)
     if out is None:
         out = torch.empty((P0, P1, n0, n1), dtype=_OUT_DTYPES[prec], device=device)
     forward_into(xt, m0, m1, out, prec=prec, scale=scale, kernel=kernel)

@@ -234,6 +234,61 @@ def test_input_kinds_widen_like_the_reference(cuda, oracle_lib):
         tree_swdft_2d([["a", "b"], ["c", "d"]], WindowSpec((1, 1)))
 
 
+def test_forward_host_c_abi(cuda, oracle_lib):
+    """swdft2d_forward_host: host array in, host array out in one C-ABI call (the call the
+    reference's numpy binding makes), strips through the 4-slot device ring."""
+    import ctypes
+
+    rng = np.random.default_rng(11)
+    xr = rng.standard_normal((90, 70))
+    ref = oracle_lib.tree2d(xr, 3, 2)                                   # (83, 67, 8, 4)
+    row_bytes = 67 * 8 * 4 * 16
+    for make in (_lib.host_empty, np.empty):                            # pinned, pageable
+        for strip in (0, row_bytes, 3 * row_bytes + 5):                 # 1, 83 and 28 strips
+            out = make(ref.shape, np.complex128)
+            out.view(np.float64).fill(np.nan)
+            _lib.forward_host(xr, 3, 2, out, prec=_lib.PREC_FP64, strip_bytes=strip)
+            assert bits_equal(out, ref)
+    # a row range of a padded view (row stride > width), scaled
+    wide = np.full((90, 96), np.nan)
+    wide[:, 5:75] = xr
+    out = _lib.host_empty((20, 67, 8, 4), np.complex128)
+    _lib.forward_host(wide[:, 5:75], 3, 2, out, prec=_lib.PREC_FP64, scale=0.125, p0_begin=31,
+                      p0_end=51, strip_bytes=2 * row_bytes)
+    assert bits_equal(out, oracle_lib.tree2d(xr, 3, 2, scale=0.125)[31:51])
+    # complex64 in fp32, and the large-window path (its workspace comes from the pool)
+    xc = (rng.standard_normal((140, 40)) + 1j * rng.standard_normal((140, 40))).astype(np.complex64)
+    out32 = _lib.host_empty((140 - 127, 39, 128, 2), np.complex64)
+    _lib.forward_host(xc, 7, 1, out32, prec=_lib.PREC_FP32, strip_bytes=4 * 39 * 256 * 8)
+    assert rel_err(out32, oracle_lib.tree2d(xc.astype(np.complex128), 7, 1)) <= FP32_TOL
+    out64 = np.empty((140 - 127, 39, 128, 2), np.complex128)
+    _lib.forward_host(xc, 7, 1, out64, prec=_lib.PREC_FP64, kernel=_lib.KERNEL_SEPARABLE)
+    assert bits_equal(out64, oracle_lib.tree2d(xc.astype(np.complex128), 7, 1))
+    # x may also be a device pointer (copied device to device)
+    xd = torch.from_numpy(xr).to(cuda)
+    out = _lib.host_empty(ref.shape, np.complex128)
+    lib = _lib.load()
+    _lib.check(lib.swdft2d_forward_host(xd.data_ptr(), _lib.IN_F64, 90, 70, 70, 3, 2, _lib.PREC_FP64,
+                                        1.0, 0, 83, out.ctypes.data, 0, _lib.KERNEL_AUTO, None))
+    assert bits_equal(out, ref)
+    # errors: null buffers, negative strip size, rows out of range; an empty range is a no-op
+    assert lib.swdft2d_forward_host(None, _lib.IN_F64, 90, 70, 70, 3, 2, _lib.PREC_FP64, 1.0, 0, 83,
+                                    out.ctypes.data, 0, 0, None) == _lib.E_INVALID_ARG
+    assert lib.swdft2d_forward_host(xr.ctypes.data, _lib.IN_F64, 90, 70, 70, 3, 2, _lib.PREC_FP64,
+                                    1.0, 0, 83, out.ctypes.data, -1, 0, None) == _lib.E_INVALID_ARG
+    assert lib.swdft2d_forward_host(xr.ctypes.data, _lib.IN_F64, 90, 70, 70, 3, 2, _lib.PREC_FP64,
+                                    1.0, 0, 84, out.ctypes.data, 0, 0, None) == _lib.E_INVALID_ARG
+    assert lib.swdft2d_forward_host(xr.ctypes.data, _lib.IN_F64, 90, 70, 70, 3, 2, _lib.PREC_FP64,
+                                    1.0, 5, 5, None, 0, 0, None) == _lib.OK
+    with pytest.raises(ValueError):
+        _lib.forward_host(xr[:, ::2], 3, 2, out, prec=_lib.PREC_FP64)
+    assert lib.swdft2d_host_free(None) == _lib.OK and not lib.swdft2d_host_alloc(0)
+    del out, out32
+    import gc
+
+    gc.collect()  # the pinned blocks are freed with their arrays (weakref.finalize)
+
+
 def test_row_ranges(cuda, oracle_lib):
     """swdft2d_forward on window-row sub-ranges (the strip boundary) is bitwise exact."""
     rng = np.random.default_rng(9)
@@ -562,8 +617,8 @@ def test_row_kernel_1d_large_and_errors(cuda, oracle_lib):
 
 
 def test_host_output_pipeline(cuda, oracle_lib):
-    """to_host / host_out: strips computed in a device ring and streamed to pinned host
-    memory equal the device-resident result bit for bit (fp64), with many strips."""
+    """to_host / host_out (one swdft2d_forward_host call): strips computed in a device ring
+    and streamed to host memory equal the oracle bit for bit (fp64), with many strips."""
     rng = np.random.default_rng(13)
     x = rng.standard_normal((70, 50)) + 1j * rng.standard_normal((70, 50))
     ref = oracle_lib.tree2d(x, 3, 2)
@@ -576,6 +631,16 @@ def test_host_output_pipeline(cuda, oracle_lib):
                           strip_bytes=1 << 12)
     assert res32.values.base is not None or res32.values.ctypes.data == host.data_ptr()
     assert rel_err(res32.values, ref) <= FP32_TOL
+    # a caller's numpy array (pageable), a device-resident input, a normalization
+    mine = np.full((63, 47, 8, 4), np.nan, dtype=np.complex128)
+    xd = torch.from_numpy(x).to(cuda)
+    res = tree_swdft_2d(xd, WindowSpec((3, 2), "unitary"), host_out=mine, strip_bytes=5 * 47 * 32 * 16)
+    assert res.values is mine and res.normalization == "unitary"
+    assert bits_equal(mine, oracle_lib.tree2d(x, 3, 2, scale=1 / np.sqrt(32)))
+    with pytest.raises(ValueError):
+        tree_swdft_2d(x, WindowSpec((3, 2)), host_out=np.empty((63, 47, 8, 4), np.complex64))
+    with pytest.raises(ValueError):
+        tree_swdft_2d(x, WindowSpec((3, 2)), host_out=np.empty((63, 47, 4, 8), np.complex128))
 
 
 @pytest.mark.parametrize("m0", list(range(0, 7)))
