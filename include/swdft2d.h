@@ -25,7 +25,9 @@
  * as void*).  Device memory: the twiddle tables and the guided K1 schedule's tile
  * counters (one 8-byte slot per stream) are allocated once per device and freed by
  * swdft2d_shutdown; a forward call allocates nothing, except the large-window path
- * when the caller gives it no workspace (see swdft2d_forward_ws).
+ * when the caller gives it no workspace (see swdft2d_forward_ws).  swdft2d_forward_host
+ * owns its device scratch (input rows + a ring of 4 output strips) and a pinned staging
+ * ring, both cached between calls and freed by swdft2d_shutdown.
  * Errors: functions return SWDFT2D_OK (0) or a negative code; the message of
  * the last error on the calling thread is swdft2d_last_error().
  */
@@ -150,9 +152,10 @@ int swdft2d_workspace_bytes(int64_t N0, int64_t N1, int m0, int m1, int prec, in
  * in strips of window rows into a ring of 4 device strips and copied out on two copy
  * streams while later strips compute, so the device holds at most 4 strips whatever the
  * output size (outputs larger than HBM are fine).  Compute is ordered on `stream`; the
- * call is synchronous: out_host is complete on return.  The device scratch (input rows +
- * ring) is taken stream-ordered from the device's default pool for the call
- * (cudaMallocAsync / cudaFreeAsync).
+ * call is synchronous: out_host is complete on return.  One host call runs at a time per
+ * process (they share the link, the scratch and the staging ring).  Pageable destinations
+ * are filled by SWDFT2D_HOST_THREADS worker threads (default: the online cores, at most 16)
+ * from SWDFT2D_HOST_CHUNK_MB-sized (default 4) pinned staging chunks.
  */
 int swdft2d_forward_host(const void *x, int in_dtype, int64_t N0, int64_t N1, int64_t ld_x, int m0,
                          int m1, int prec, double scale, int64_t p0_begin, int64_t p0_end,
@@ -256,7 +259,8 @@ int swdft2d_forward_columns(const void *z, int prec, int64_t N0, int64_t cols, i
                             int m_inner, double scale, int64_t p0_begin, int64_t p0_end, void *out,
                             void *stream);
 
-/* Frees cached per-device state (twiddle tables, tile counters).  Safe to call twice;
+/* Frees cached per-device state (twiddle tables, tile counters, swdft2d_forward_host's
+ * device scratch and pinned staging).  Safe to call twice;
  * no call may be in flight on any stream. */
 int swdft2d_shutdown(void);
 

@@ -291,7 +291,7 @@ int swdft2d_forward_host(const void *x, int in_dtype, int64_t N0, int64_t N1, in
     if (!direct) {
         long cores = sysconf(_SC_NPROCESSORS_ONLN);
         const int slots = env_int("SWDFT2D_HOST_THREADS", cores > 16 ? 16 : cores < 2 ? 2 : (int)cores, 1, 64);
-        const size_t chunk = (size_t)env_int("SWDFT2D_HOST_CHUNK_MB", 8, 1, 256) << 20;
+        const size_t chunk = (size_t)env_int("SWDFT2D_HOST_CHUNK_MB", 4, 1, 256) << 20;
         void *pin = nullptr;
         if ((e = staging(slots * chunk, &pin)) != cudaSuccess) {
             cudaGetLastError();

@@ -251,3 +251,46 @@ def test_reference_1d_kd_entry_points(swdft, cuda, tmp_path):
         finally:
             swdft_b200.enable()
     assert outs["b200"] == outs["numpy"]
+
+
+STUB = r"""
+import ctypes, os, sys
+import numpy as np
+sys.path.insert(0, {root!r})
+import oracle                                     # the checker (numpy + C, no torch)
+
+lib = ctypes.CDLL({lib!r})
+i64, cint, vp = ctypes.c_int64, ctypes.c_int, ctypes.c_void_p
+lib.swdft2d_forward_host.argtypes = [vp, cint, i64, i64, i64, cint, cint, cint, ctypes.c_double,
+                                     i64, i64, vp, i64, cint, vp]
+lib.swdft2d_forward_host.restype = cint
+lib.swdft2d_last_error.restype = ctypes.c_char_p
+rng = np.random.default_rng(21)
+x = np.ascontiguousarray(rng.standard_normal((300, 200)) + 1j * rng.standard_normal((300, 200)))
+m0, m1 = 4, 3
+out = np.empty((300 - 15, 200 - 7, 16, 8), dtype=np.complex128)
+rc = lib.swdft2d_forward_host(x.ctypes.data, 3, 300, 200, 200, m0, m1, 1, 1.0, 0, 285,
+                              out.ctypes.data, 1 << 22, 0, None)
+assert rc == 0, lib.swdft2d_last_error()
+ref = oracle.tree2d(x, m0, m1)
+assert np.array_equal(out.view(np.uint64), ref.view(np.uint64))
+rc = lib.swdft2d_forward_host(x.ctypes.data, 3, 300, 200, 200, 9, m1, 1, 1.0, 0, 1,
+                              out.ctypes.data, 0, 0, None)
+assert rc == -3 and b"window" in lib.swdft2d_last_error().lower()   # WindowTooLargeError
+assert "torch" not in sys.modules
+print("stub ok")
+"""
+
+
+@pytest.mark.gpu
+def test_ctypes_stub_needs_no_torch(oracle_lib):
+    """INTEGRATION.md's stub as a maintainer would write it: numpy + ctypes only, one
+    swdft2d_forward_host call on numpy buffers, in a process that never imports torch
+    (the library brings its own CUDA runtime); bitwise equal to the oracle."""
+    import subprocess
+
+    from paper_1707_08213_b200 import _lib
+
+    code = STUB.format(root=ROOT, lib=_lib.LIB_PATH)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "stub ok" in r.stdout, r.stdout + r.stderr
