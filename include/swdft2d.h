@@ -161,6 +161,14 @@ int swdft2d_forward_host(const void *x, int in_dtype, int64_t N0, int64_t N1, in
                          int m1, int prec, double scale, int64_t p0_begin, int64_t p0_end,
                          void *out_host, int64_t strip_bytes, int kernel, void *stream);
 
+/*
+ * Device buffer -> host array, synchronous, ordered after the work queued on `stream`
+ * (results that were left resident, the 1D / kD outputs).  Pinned destinations take one
+ * cudaMemcpyAsync; pageable ones (a fresh numpy array) go through the same pinned staging
+ * ring and worker threads as swdft2d_forward_host.
+ */
+int swdft2d_download(const void *dev_src, void *host_dst, int64_t bytes, void *stream);
+
 /* Pinned (page-locked, portable) host memory for swdft2d_forward_host's buffers; NULL on
  * failure (swdft2d_last_error).  Free with swdft2d_host_free. */
 void *swdft2d_host_alloc(int64_t bytes);

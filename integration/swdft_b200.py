@@ -104,7 +104,11 @@ def tree_swdft_2d_b200(x, spec, loop_order: str = "levels-outer", counter=None,
 
 
 def _host_or_device(values):
-    return values if _STATE["values"] == "device" else values.cpu().numpy()
+    if _STATE["values"] == "device":
+        return values
+    from paper_1707_08213_b200 import _lib
+
+    return _lib.download(values)  # swdft2d_download: staged, not a pageable cudaMemcpy
 
 
 def tree_swdft_1d_b200(x, spec, counter=None):

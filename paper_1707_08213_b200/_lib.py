@@ -48,6 +48,7 @@ SIGNATURES = {
                                   _i64, _vp, _vp, _i64, _int, _vp]),
     "swdft2d_forward_host": (_int, [_vp, _int, _i64, _i64, _i64, _int, _int, _int, _dbl, _i64,
                                     _i64, _vp, _i64, _int, _vp]),
+    "swdft2d_download": (_int, [_vp, _vp, _i64, _vp]),
     "swdft2d_host_alloc": (_vp, [_i64]),
     "swdft2d_host_free": (_int, [_vp]),
     "swdft2d_workspace_bytes": (_int, [_i64, _i64, _int, _int, _int, _i64, _i64, _int, _pi64]),
@@ -235,4 +236,21 @@ def forward_host(x, m0: int, m1: int, out, *, prec: int, scale: float = 1.0, p0_
     check(load().swdft2d_forward_host(x.ctypes.data, code, N0, N1, ld, m0,
                                       m1, prec, float(scale), p0_begin, p0_end, out.ctypes.data,
                                       strip_bytes, kernel, stream))
+    return out
+
+
+def download(t):
+    """CUDA tensor -> fresh numpy array through swdft2d_download (staged by worker threads:
+    several times the rate of ``t.cpu()`` into fresh pageable memory)."""
+    import numpy as np
+    import torch
+
+    if not t.is_cuda:
+        return t.numpy()
+    t = t.contiguous()
+    out = np.empty(tuple(t.shape), dtype=torch.empty((), dtype=t.dtype).numpy().dtype)
+    if out.nbytes:
+        with torch.cuda.device(t.device):
+            check(load().swdft2d_download(t.data_ptr(), out.ctypes.data, out.nbytes,
+                                          raw_stream(t.device.index)))
     return out

@@ -157,6 +157,15 @@ class CoefficientArray:
     def positions(self) -> tuple:
         return tuple(N - n + 1 for N, n in zip(self.source_shape, self.window.sizes))
 
+    def numpy(self):
+        """``values`` as a numpy array, the reference's own return type: a device tensor
+        is copied out through swdft2d_download (pinned staging + worker threads)."""
+        if hasattr(self.values, "is_cuda"):
+            from . import _lib
+
+            return _lib.download(self.values)
+        return self.values
+
 
 def output_elements(shape: Sequence[int], spec) -> int:
     spec.check_fits(shape)

@@ -198,6 +198,22 @@ bool is_pinned(const void *p) {
     return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
 }
 
+// The staging workers for a pageable destination (SWDFT2D_HOST_THREADS slots of
+// SWDFT2D_HOST_CHUNK_MB MiB; the pinned ring is cached).
+int make_stager(int dev, Stager **out) {
+    long cores = sysconf(_SC_NPROCESSORS_ONLN);
+    const int slots = env_int("SWDFT2D_HOST_THREADS", cores > 16 ? 16 : cores < 2 ? 2 : (int)cores, 1, 64);
+    const size_t chunk = (size_t)env_int("SWDFT2D_HOST_CHUNK_MB", 4, 1, 256) << 20;
+    void *pin = nullptr;
+    cudaError_t e = staging(slots * chunk, &pin);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(SWDFT2D_E_NOMEM, "pinned staging (%zu B): %s", slots * chunk, cudaGetErrorString(e));
+    }
+    *out = new Stager(dev, static_cast<char *>(pin), slots, chunk);
+    return SWDFT2D_OK;
+}
+
 }  // namespace
 
 void release_host_pipe() {
@@ -241,6 +257,47 @@ int swdft2d_host_free(void *p) {
     if (!p) return SWDFT2D_OK;
     cudaError_t e = cudaFreeHost(p);
     if (e != cudaSuccess) return set_error(SWDFT2D_E_CUDA, "cudaFreeHost: %s", cudaGetErrorString(e));
+    return SWDFT2D_OK;
+}
+
+int swdft2d_download(const void *dev_src, void *host_dst, int64_t bytes, void *stream) {
+    if (bytes < 0) return set_error(SWDFT2D_E_INVALID_ARG, "download: %lld bytes", (long long)bytes);
+    if (bytes == 0) return SWDFT2D_OK;
+    if (!dev_src || !host_dst) return set_error(SWDFT2D_E_INVALID_ARG, "null pointer");
+    std::lock_guard<std::mutex> call(g_call_mu);
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return set_error(SWDFT2D_E_CUDA, "cudaGetDevice: %s", cudaGetErrorString(e));
+    Pipe pipe;
+    if ((e = pipe.init()) != cudaSuccess)
+        return set_error(SWDFT2D_E_CUDA, "download: streams/events: %s", cudaGetErrorString(e));
+    // the copy stream waits for the work already queued on the caller's stream
+    e = cudaEventRecord(pipe.done[0], reinterpret_cast<cudaStream_t>(stream));
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(pipe.copy[0], pipe.done[0], 0);
+    const char *src = static_cast<const char *>(dev_src);
+    char *dst = static_cast<char *>(host_dst);
+    if (is_pinned(host_dst)) {
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToHost, pipe.copy[0]);
+    } else {
+        Stager *stager = nullptr;
+        int rc = make_stager(dev, &stager);
+        if (rc) return rc;
+        int64_t index = 0;
+        for (size_t off = 0; off < (size_t)bytes && e == cudaSuccess; off += stager->chunk()) {
+            const size_t n = (size_t)bytes - off < stager->chunk() ? (size_t)bytes - off : stager->chunk();
+            e = stager->submit(index++, src + off, dst + off, n, pipe.copy[0]);
+        }
+        cudaError_t e2 = stager->finish();
+        if (e == cudaSuccess) e = e2;
+        delete stager;
+    }
+    cudaError_t e3 = cudaStreamSynchronize(pipe.copy[0]);
+    if (e == cudaSuccess) e = e3;
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(SWDFT2D_E_CUDA, "download: %s", cudaGetErrorString(e));
+    }
     return SWDFT2D_OK;
 }
 
@@ -288,18 +345,7 @@ int swdft2d_forward_host(const void *x, int in_dtype, int64_t N0, int64_t N1, in
     // pageable destination: pinned staging ring + one worker per slot
     const bool direct = is_pinned(out_host);
     Stager *stager = nullptr;
-    if (!direct) {
-        long cores = sysconf(_SC_NPROCESSORS_ONLN);
-        const int slots = env_int("SWDFT2D_HOST_THREADS", cores > 16 ? 16 : cores < 2 ? 2 : (int)cores, 1, 64);
-        const size_t chunk = (size_t)env_int("SWDFT2D_HOST_CHUNK_MB", 4, 1, 256) << 20;
-        void *pin = nullptr;
-        if ((e = staging(slots * chunk, &pin)) != cudaSuccess) {
-            cudaGetLastError();
-            return set_error(SWDFT2D_E_NOMEM, "forward_host: pinned staging (%zu B): %s", slots * chunk,
-                             cudaGetErrorString(e));
-        }
-        stager = new Stager(dev, static_cast<char *>(pin), slots, chunk);
-    }
+    if (!direct && (rc = make_stager(dev, &stager))) return rc;
 
     e = cudaMemcpy2DAsync(d_x, (size_t)(N1 * es), static_cast<const char *>(x) + p0_begin * ld_x * es,
                           (size_t)(ld_x * es), (size_t)(N1 * es), (size_t)rows_in, cudaMemcpyDefault, st);

@@ -92,6 +92,12 @@ def main():
         t = time.perf_counter() - t0
         res["device+cpu"] = {"s": t, "gcoef_s": c.coefficients / t / 1e9}
         assert np.array_equal(chk, v[c.P0 // 2, c.P1 // 3])
+        del v
+        t0 = time.perf_counter()
+        v = r.numpy()  # swdft2d_download: staged by worker threads
+        t = time.perf_counter() - t0
+        res["download_fresh"] = {"s": t, "gb_s": v.nbytes / t / 1e9}
+        assert np.array_equal(chk, v[c.P0 // 2, c.P1 // 3])
     print(json.dumps(res), flush=True)
 
 

@@ -289,6 +289,31 @@ def test_forward_host_c_abi(cuda, oracle_lib):
     gc.collect()  # the pinned blocks are freed with their arrays (weakref.finalize)
 
 
+def test_download_and_numpy_helper(cuda):
+    """swdft2d_download: device tensor -> pinned or pageable host array (the latter through
+    the staging workers, several chunks, an odd tail), ordered after the producing stream."""
+    g = torch.Generator(device=cuda).manual_seed(3)
+    t = torch.randn((9, 1237, 257), dtype=torch.float64, device=cuda, generator=g)
+    c = torch.view_as_complex(t[..., :256].reshape(9, 1237, 128, 2).contiguous())   # 18 MB
+    ref = c.cpu().numpy()
+    got = _lib.download(c)
+    assert got.dtype == np.complex128 and got.shape == ref.shape and bits_equal(got, ref)
+    pinned = _lib.host_empty(ref.shape, np.complex128)
+    _lib.check(_lib.load().swdft2d_download(c.data_ptr(), pinned.ctypes.data, pinned.nbytes, None))
+    assert bits_equal(pinned, ref)
+    assert _lib.download(c[:, ::3]).shape == (9, 413, 128)                # non-contiguous view
+    assert _lib.download(torch.empty((0, 4), dtype=torch.complex64, device=cuda)).shape == (0, 4)
+    s = torch.cuda.Stream(cuda)
+    with torch.cuda.stream(s):                                            # stream ordering
+        big = torch.zeros(1 << 24, dtype=torch.float32, device=cuda)
+        for _ in range(20):
+            big += 1.0
+        assert float(_lib.download(big)[-1]) == 20.0
+    res = tree_swdft_2d(np.ones((8, 8)), WindowSpec((2, 2)), budget=1 << 30)
+    assert isinstance(res.numpy(), np.ndarray) and bits_equal(res.numpy(), res.values.cpu().numpy())
+    assert _lib.load().swdft2d_download(None, pinned.ctypes.data, 8, None) == _lib.E_INVALID_ARG
+
+
 def test_row_ranges(cuda, oracle_lib):
     """swdft2d_forward on window-row sub-ranges (the strip boundary) is bitwise exact."""
     rng = np.random.default_rng(9)
