@@ -47,6 +47,52 @@ int env_int(const char *name, int dflt, int lo, int hi) {
     return v < lo ? lo : v > hi ? hi : v;
 }
 
+// Staging chunk -> destination.  Non-temporal stores: the destination is written once and
+// not read back by this core, so regular stores would first read every line for ownership
+// (SWDFT2D_HOST_NT=0 falls back to memcpy; x86-64 with AVX2 only).
+#if defined(__x86_64__)
+#include <immintrin.h>
+__attribute__((target("avx2"))) void nt_copy_avx2(char *dst, const char *src, size_t len) {
+    size_t head = (32 - ((uintptr_t)dst & 31)) & 31;
+    if (head > len) head = len;
+    std::memcpy(dst, src, head);
+    dst += head;
+    src += head;
+    len -= head;
+    size_t i = 0;
+    for (; i + 128 <= len; i += 128) {
+        const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i *>(src + i));
+        const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i *>(src + i + 32));
+        const __m256i c = _mm256_loadu_si256(reinterpret_cast<const __m256i *>(src + i + 64));
+        const __m256i d = _mm256_loadu_si256(reinterpret_cast<const __m256i *>(src + i + 96));
+        _mm256_stream_si256(reinterpret_cast<__m256i *>(dst + i), a);
+        _mm256_stream_si256(reinterpret_cast<__m256i *>(dst + i + 32), b);
+        _mm256_stream_si256(reinterpret_cast<__m256i *>(dst + i + 64), c);
+        _mm256_stream_si256(reinterpret_cast<__m256i *>(dst + i + 96), d);
+    }
+    _mm_sfence();
+    std::memcpy(dst + i, src + i, len - i);
+}
+#endif
+
+void copy_out(char *dst, const char *src, size_t len, bool nt) {
+#if defined(__x86_64__)
+    if (nt) {
+        nt_copy_avx2(dst, src, len);
+        return;
+    }
+#endif
+    std::memcpy(dst, src, len);
+}
+
+bool use_nt() {
+#if defined(__x86_64__)
+    return env_int("SWDFT2D_HOST_NT", 1, 0, 1) && __builtin_cpu_supports("avx2");
+#else
+    return false;
+#endif
+}
+
 // One host-to-host call at a time: calls share the link, the scratch and the staging ring.
 std::mutex g_call_mu;
 std::map<int, std::pair<void *, size_t>> g_scratch;  // device -> cached scratch
@@ -118,11 +164,12 @@ struct Pipe {
 class Stager {
   public:
     Stager(int dev, char *pinned, int slots, size_t chunk) : chunk_(chunk), slots_(slots) {
+        const bool nt = use_nt();
         for (int i = 0; i < slots; ++i) {
             Slot *s = &slots_[i];
             s->pin = pinned + (size_t)i * chunk;
             s->err = cudaEventCreateWithFlags(&s->ev, cudaEventDisableTiming);
-            s->th = std::thread([s, dev] {
+            s->th = std::thread([s, dev, nt] {
                 cudaSetDevice(dev);
                 std::unique_lock<std::mutex> lk(s->m);
                 for (;;) {
@@ -130,7 +177,7 @@ class Stager {
                     if (!s->busy) return;
                     lk.unlock();
                     cudaError_t e = cudaEventSynchronize(s->ev);
-                    if (e == cudaSuccess) std::memcpy(s->dst, s->pin, s->len);
+                    if (e == cudaSuccess) copy_out(s->dst, s->pin, s->len, nt);
                     lk.lock();
                     if (e != cudaSuccess && s->err == cudaSuccess) s->err = e;
                     s->busy = false;
