@@ -25,6 +25,7 @@
 #include <condition_variable>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <map>
 #include <mutex>
 #include <thread>
@@ -236,13 +237,15 @@ class Stager {
     std::vector<Slot> slots_;
 };
 
-bool is_pinned(const void *p) {
+enum HostKind { PAGEABLE, PINNED, DEVICE };
+HostKind host_kind(const void *p) {
     cudaPointerAttributes a;
     if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
         cudaGetLastError();
-        return false;
+        return PAGEABLE;
     }
-    return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+    if (a.type == cudaMemoryTypeDevice) return DEVICE;
+    return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged ? PINNED : PAGEABLE;
 }
 
 // The staging workers for a pageable destination (SWDFT2D_HOST_THREADS slots of
@@ -257,7 +260,11 @@ int make_stager(int dev, Stager **out) {
         cudaGetLastError();
         return set_error(SWDFT2D_E_NOMEM, "pinned staging (%zu B): %s", slots * chunk, cudaGetErrorString(e));
     }
-    *out = new Stager(dev, static_cast<char *>(pin), slots, chunk);
+    try {
+        *out = new Stager(dev, static_cast<char *>(pin), slots, chunk);
+    } catch (const std::exception &ex) {  // thread creation refused
+        return set_error(SWDFT2D_E_NOMEM, "staging workers: %s", ex.what());
+    }
     return SWDFT2D_OK;
 }
 
@@ -311,6 +318,8 @@ int swdft2d_download(const void *dev_src, void *host_dst, int64_t bytes, void *s
     if (bytes < 0) return set_error(SWDFT2D_E_INVALID_ARG, "download: %lld bytes", (long long)bytes);
     if (bytes == 0) return SWDFT2D_OK;
     if (!dev_src || !host_dst) return set_error(SWDFT2D_E_INVALID_ARG, "null pointer");
+    const HostKind kind = host_kind(host_dst);
+    if (kind == DEVICE) return set_error(SWDFT2D_E_INVALID_ARG, "download: host_dst is a device pointer");
     std::lock_guard<std::mutex> call(g_call_mu);
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
@@ -323,7 +332,7 @@ int swdft2d_download(const void *dev_src, void *host_dst, int64_t bytes, void *s
     if (e == cudaSuccess) e = cudaStreamWaitEvent(pipe.copy[0], pipe.done[0], 0);
     const char *src = static_cast<const char *>(dev_src);
     char *dst = static_cast<char *>(host_dst);
-    if (is_pinned(host_dst)) {
+    if (kind == PINNED) {
         if (e == cudaSuccess)
             e = cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToHost, pipe.copy[0]);
     } else {
@@ -360,6 +369,9 @@ int swdft2d_forward_host(const void *x, int in_dtype, int64_t N0, int64_t N1, in
     if (rc) return rc;
     if (p0_begin == p0_end) return SWDFT2D_OK;
     if (!x || !out_host) return set_error(SWDFT2D_E_INVALID_ARG, "null pointer");
+    const HostKind kind = host_kind(out_host);
+    if (kind == DEVICE)
+        return set_error(SWDFT2D_E_INVALID_ARG, "forward_host: out_host is a device pointer (use swdft2d_forward)");
     if (strip_bytes < 0) return set_error(SWDFT2D_E_INVALID_ARG, "strip_bytes %lld", (long long)strip_bytes);
     if (strip_bytes == 0) strip_bytes = (int64_t)512 << 20;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -390,7 +402,7 @@ int swdft2d_forward_host(const void *x, int in_dtype, int64_t N0, int64_t N1, in
     char *d_x = static_cast<char *>(scratch), *ring = d_x + in_bytes;
 
     // pageable destination: pinned staging ring + one worker per slot
-    const bool direct = is_pinned(out_host);
+    const bool direct = kind == PINNED;
     Stager *stager = nullptr;
     if (!direct && (rc = make_stager(dev, &stager))) return rc;
 

@@ -280,6 +280,9 @@ def test_forward_host_c_abi(cuda, oracle_lib):
                                     1.0, 0, 84, out.ctypes.data, 0, 0, None) == _lib.E_INVALID_ARG
     assert lib.swdft2d_forward_host(xr.ctypes.data, _lib.IN_F64, 90, 70, 70, 3, 2, _lib.PREC_FP64,
                                     1.0, 5, 5, None, 0, 0, None) == _lib.OK
+    dout = torch.empty(ref.shape, dtype=torch.complex128, device=cuda)   # a device pointer is refused
+    assert lib.swdft2d_forward_host(xr.ctypes.data, _lib.IN_F64, 90, 70, 70, 3, 2, _lib.PREC_FP64,
+                                    1.0, 0, 83, dout.data_ptr(), 0, 0, None) == _lib.E_INVALID_ARG
     with pytest.raises(ValueError):
         _lib.forward_host(xr[:, ::2], 3, 2, out, prec=_lib.PREC_FP64)
     assert lib.swdft2d_host_free(None) == _lib.OK and not lib.swdft2d_host_alloc(0)
