@@ -40,6 +40,7 @@ namespace {
 constexpr int RING = 4;     // device strips in flight
 constexpr int COPIERS = 2;  // copy streams
 constexpr int64_t IN_BYTES[4] = {4, 8, 8, 16};
+constexpr int64_t SMALL_DIRECT_BYTES = 16 << 20;  // pageable outputs up to here: plain copies
 
 int env_int(const char *name, int dflt, int lo, int hi) {
     const char *e = std::getenv(name);
@@ -332,7 +333,7 @@ int swdft2d_download(const void *dev_src, void *host_dst, int64_t bytes, void *s
     if (e == cudaSuccess) e = cudaStreamWaitEvent(pipe.copy[0], pipe.done[0], 0);
     const char *src = static_cast<const char *>(dev_src);
     char *dst = static_cast<char *>(host_dst);
-    if (kind == PINNED) {
+    if (kind == PINNED || bytes <= SMALL_DIRECT_BYTES) {
         if (e == cudaSuccess)
             e = cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToHost, pipe.copy[0]);
     } else {
@@ -402,7 +403,9 @@ int swdft2d_forward_host(const void *x, int in_dtype, int64_t N0, int64_t N1, in
     char *d_x = static_cast<char *>(scratch), *ring = d_x + in_bytes;
 
     // pageable destination: pinned staging ring + one worker per slot
-    const bool direct = kind == PINNED;
+    // small pageable outputs are not worth a set of worker threads: the driver's own
+    // staged copy handles them
+    const bool direct = kind == PINNED || rows * row_bytes <= SMALL_DIRECT_BYTES;
     Stager *stager = nullptr;
     if (!direct && (rc = make_stager(dev, &stager))) return rc;
 
