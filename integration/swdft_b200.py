@@ -24,6 +24,11 @@ swdft/tree2d.py:175-202``) gets:
   * the same ``counter.add_region`` calls as ``_levels_outer`` (``tree2d.py:90-92,
     115-118``), replayed from the reference's own ``core.shift_schedule``.
 
+The stream classes ``swdft.tree2d.SlidingRowStream2D`` (``tree2d.py:205-303``) and
+``swdft.tree1d.SlidingStream1D`` (``tree1d.py:63-119``) are routed too: same constructors,
+attributes, exceptions and per-push accounting, slabs / vectors bitwise equal to the batch
+transform's rows.
+
 ``values`` is a numpy array, as the reference returns, unless ``enable(values="device")``
 (then a CUDA tensor stays in HBM; ``CoefficientArray`` accepts it).  ``loop_order`` is
 validated and then has no effect (the reference's two orders are bitwise identical);
@@ -147,15 +152,100 @@ def tree_swdft_kd_b200(x, spec, counter=None, budget=None):
     return core.CoefficientArray(_host_or_device(r.values), x.shape, spec, spec.normalization)
 
 
+def _translate(exc):
+    """This package's exception -> the reference's class of the same name (core.py:23-56)."""
+    from swdft import core
+
+    cls = getattr(core, type(exc).__name__, None)
+    return cls(*exc.args) if isinstance(cls, type) and issubclass(cls, Exception) else exc
+
+
+class SlidingRowStream2D_b200:
+    """swdft.tree2d.SlidingRowStream2D (tree2d.py:205-303) on the B200: same constructor,
+    attributes, exceptions, per-push operation accounting and counter calls; ``push_row``
+    returns the (P1, n0, n1) slab (numpy, or a CUDA tensor with ``enable(values="device")``),
+    bitwise equal to the batch transform's rows in fp64 (SPEC.md:343).  The reference's own
+    class raises for every window larger than 1x1 (SURVEY.md App. A #11)."""
+
+    def __init__(self, spec, row_length: int, counter=None):
+        from swdft import core
+
+        from paper_1707_08213_b200 import stream as b200_stream
+
+        if spec.k != 2:  # tree2d.py:217-226, the reference's own checks
+            raise core.ShapeError("SlidingRowStream2D needs a 2D window spec")
+        if spec.sizes[1] > int(row_length):
+            raise core.WindowTooLargeError(
+                f"window size {spec.sizes[1]} exceeds row length {int(row_length)}")
+        self._s = b200_stream.SlidingRowStream2D(spec, row_length, counter,
+                                                 precision=_STATE["precision"],
+                                                 device=_STATE["device"])
+        self.spec, self.counter = spec, counter
+        self.m0, self.m1 = spec.exponents
+        self.n0, self.n1 = spec.sizes
+        self.N1 = int(row_length)
+
+    rows_pushed = property(lambda self: self._s.rows_pushed)
+    ops_last_push = property(lambda self: self._s.ops_last_push)
+    last_push_position_ops = property(lambda self: self._s.last_push_position_ops)
+    closed = property(lambda self: self._s.closed)
+
+    def push_row(self, row):
+        import numpy as np
+
+        try:
+            slab = self._s.push_row(np.asarray(row, dtype=np.complex128))
+        except Exception as e:  # noqa: BLE001
+            raise _translate(e) from None
+        return None if slab is None else _host_or_device(slab)
+
+    def close(self) -> None:
+        self._s.close()
+
+
+class SlidingStream1D_b200:
+    """swdft.tree1d.SlidingStream1D (tree1d.py:63-119) on the B200."""
+
+    def __init__(self, spec, counter=None):
+        from swdft import core
+
+        from paper_1707_08213_b200 import stream as b200_stream
+
+        if spec.k != 1:
+            raise core.ShapeError("SlidingStream1D needs a 1D window spec")
+        self._s = b200_stream.SlidingStream1D(spec, counter, precision=_STATE["precision"],
+                                              device=_STATE["device"])
+        self.spec, self.counter = spec, counter
+        (self.m,) = spec.exponents
+        (self.n,) = spec.sizes
+
+    pushed = property(lambda self: self._s.pushed)
+    ops_last_push = property(lambda self: self._s.ops_last_push)
+    closed = property(lambda self: self._s.closed)
+
+    def push(self, sample):
+        try:
+            out = self._s.push(sample)
+        except Exception as e:  # noqa: BLE001
+            raise _translate(e) from None
+        return None if out is None else _host_or_device(out)
+
+    def close(self) -> None:
+        self._s.close()
+
+
 # (module, attribute, B200 function) the binding routes
 _ROUTES = (("tree2d", "tree_swdft_2d", tree_swdft_2d_b200),
            ("tree1d", "tree_swdft_1d", tree_swdft_1d_b200),
-           ("treekd", "tree_swdft_kd", tree_swdft_kd_b200))
+           ("treekd", "tree_swdft_kd", tree_swdft_kd_b200),
+           ("tree2d", "SlidingRowStream2D", SlidingRowStream2D_b200),
+           ("tree1d", "SlidingStream1D", SlidingStream1D_b200))
 
 
 def enable(values: str = "numpy", precision: str = "fp64", device=None) -> None:
-    """Route swdft.tree2d.tree_swdft_2d, swdft.tree1d.tree_swdft_1d and
-    swdft.treekd.tree_swdft_kd to libswdft2d.so (idempotent).
+    """Route swdft.tree2d.tree_swdft_2d, swdft.tree1d.tree_swdft_1d,
+    swdft.treekd.tree_swdft_kd and the two stream classes (tree2d.SlidingRowStream2D,
+    tree1d.SlidingStream1D) to libswdft2d.so (idempotent).
 
     values     "numpy" (the reference's return type) or "device" (a CUDA tensor)
     precision  "fp64" (complex128, bitwise equal to the reference) or "fp32"
@@ -178,7 +268,7 @@ def enable(values: str = "numpy", precision: str = "fp64", device=None) -> None:
             mod = importlib.import_module("swdft." + modname)
             orig = getattr(mod, attr)
             _STATE["origs"][(modname, attr)] = orig
-            setattr(mod, attr, functools.wraps(orig)(fn))
+            setattr(mod, attr, fn if isinstance(fn, type) else functools.wraps(orig)(fn))
 
 
 def disable() -> None:

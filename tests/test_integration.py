@@ -253,6 +253,79 @@ def test_reference_1d_kd_entry_points(swdft, cuda, tmp_path):
     assert outs["b200"] == outs["numpy"]
 
 
+@pytest.mark.gpu
+def test_reference_stream_classes(swdft, cuda):
+    """swdft.tree2d.SlidingRowStream2D and swdft.tree1d.SlidingStream1D routed to the B200:
+    the reference's exceptions and attributes; 2-D slabs bitwise equal to the rows of the
+    reference's own batch transform (its own stream raises for windows above 1x1, App. A
+    #11, and is compared where it runs: 1x1); 1-D vectors, per-push ops and counters bitwise
+    / exactly equal to the reference's own 1-D stream."""
+    import swdft.tree1d
+
+    import swdft_b200
+
+    core, bench, tree2d = swdft.core, swdft.bench, swdft.tree2d
+    rng = np.random.default_rng(33)
+    batch = swdft_b200.original("tree2d", "tree_swdft_2d")
+    for (N0, N1), exps, mode in (((20, 17), (2, 3), "none"), ((12, 9), (3, 0), "unitary"),
+                                 ((70, 40), (5, 2), "none")):
+        x = rng.standard_normal((N0, N1)) + 1j * rng.standard_normal((N0, N1))
+        spec = core.WindowSpec(exps, mode)
+        n0, n1 = spec.sizes
+        ref = batch(x, spec, budget=1 << 40).values
+        cnt = bench.OpCounter((N0, N1))
+        st = tree2d.SlidingRowStream2D(spec, N1, counter=cnt)
+        assert type(st).__name__ == "SlidingRowStream2D_b200" and st.n0 == n0 and st.N1 == N1
+        for r in range(N0):
+            slab = st.push_row(x[r])
+            assert st.rows_pushed == r + 1
+            if r < n0 - 1:
+                assert slab is None
+            else:
+                assert isinstance(slab, np.ndarray) and slab.shape == (N1 - n1 + 1, n0, n1)
+                assert np.array_equal(slab.view(np.uint64),
+                                      np.ascontiguousarray(ref[r - n0 + 1]).view(np.uint64))
+                assert st.last_push_position_ops[-1] == 2 * (n0 * n1 - 1)   # SPEC acceptance 7
+        cb = bench.OpCounter((N0, N1))
+        batch(x, spec, counter=cb, budget=1 << 40)
+        assert cnt.total == cb.total and np.array_equal(cnt.position_ops, cb.position_ops)
+        with pytest.raises(core.ShapeError):
+            st.push_row(np.zeros(N1 + 1))
+        st.close()
+        assert st.closed
+        with pytest.raises(core.StateError):
+            st.push_row(x[0])
+    with pytest.raises(core.ShapeError):
+        tree2d.SlidingRowStream2D(core.WindowSpec((2,)), 8)
+    with pytest.raises(core.WindowTooLargeError):
+        tree2d.SlidingRowStream2D(core.WindowSpec((1, 4)), 8)
+    # 1x1 windows: the one case the reference's own 2-D stream runs
+    RefStream = swdft_b200.original("tree2d", "SlidingRowStream2D")
+    spec = core.WindowSpec((0, 0))
+    a, b = RefStream(spec, 6), tree2d.SlidingRowStream2D(spec, 6)
+    for r in range(4):
+        row = rng.standard_normal(6)
+        ra, rb = a.push_row(row), b.push_row(row)
+        assert np.array_equal(ra.view(np.uint64), rb.view(np.uint64))
+        assert a.ops_last_push == b.ops_last_push
+    # 1-D stream vs the reference's own
+    Ref1 = swdft_b200.original("tree1d", "SlidingStream1D")
+    for m, mode in ((3, "none"), (6, "unitary"), (0, "none"), (7, "none")):
+        spec = core.WindowSpec((m,), mode)
+        ca, cb = bench.OpCounter((200,)), bench.OpCounter((200,))
+        a, b = Ref1(spec, counter=ca), swdft.tree1d.SlidingStream1D(spec, counter=cb)
+        for p in range(200):
+            v = complex(rng.standard_normal(), rng.standard_normal())
+            ra, rb = a.push(v), b.push(v)
+            assert (ra is None) == (rb is None) and a.ops_last_push == b.ops_last_push
+            if ra is not None:
+                assert np.array_equal(ra.view(np.uint64), rb.view(np.uint64)), (m, p)
+        assert ca.total == cb.total and b.pushed == 200
+        b.close()
+        with pytest.raises(core.StateError):
+            b.push(0.0)
+
+
 STUB = r"""
 import ctypes, os, sys
 import numpy as np
