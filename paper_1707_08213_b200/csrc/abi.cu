@@ -1155,6 +1155,9 @@ int swdft2d_forward_columns(const void *z, int prec, int64_t N0, int64_t cols, i
 }
 
 int swdft2d_shutdown(void) {
+    // the host path first, outside g_mu: a host-to-host call holds its own lock and then
+    // takes g_mu inside the forward calls it makes (same order here)
+    release_host_pipe();
     std::lock_guard<std::mutex> lk(g_mu);
     int cur = 0;
     cudaGetDevice(&cur);
@@ -1170,7 +1173,6 @@ int swdft2d_shutdown(void) {
         }
     }
     g_dev.clear();
-    release_host_pipe();
     cudaSetDevice(cur);
     return SWDFT2D_OK;
 }

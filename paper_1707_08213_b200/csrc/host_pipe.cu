@@ -167,6 +167,17 @@ class Stager {
   public:
     Stager(int dev, char *pinned, int slots, size_t chunk) : chunk_(chunk), slots_(slots) {
         const bool nt = use_nt();
+        try {
+            start(dev, pinned, slots, chunk, nt);
+        } catch (...) {  // a thread could not be created: stop the ones that were
+            finish();
+            throw;
+        }
+    }
+    size_t chunk() const { return chunk_; }
+
+  private:
+    void start(int dev, char *pinned, int slots, size_t chunk, bool nt) {
         for (int i = 0; i < slots; ++i) {
             Slot *s = &slots_[i];
             s->pin = pinned + (size_t)i * chunk;
@@ -188,7 +199,8 @@ class Stager {
             });
         }
     }
-    size_t chunk() const { return chunk_; }
+
+  public:
     cudaError_t submit(int64_t index, const char *dev_src, char *dst, size_t len, cudaStream_t cs) {
         Slot *s = &slots_[index % (int64_t)slots_.size()];
         std::unique_lock<std::mutex> lk(s->m);
