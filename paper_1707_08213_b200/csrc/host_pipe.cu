@@ -14,7 +14,8 @@
 //     memcpy run on many cores while the link keeps streaming (config 4, 34 GB, 16 cores:
 //     1.0 s into a fresh numpy array, 0.65-0.72 s into touched pages, against 10.1 s /
 //     1.7 s for the driver's pageable copy and 0.61 s pinned; MADV_HUGEPAGE on the
-//     destination measured level to 10 % slower and is not used;
+//     destination measured level to 10 % slower and MADV_POPULATE_WRITE per chunk level
+//     (alternated runs: 1.16-1.38 vs 1.13-1.20 s), neither is used;
 //     profiles/host_entry_r02.jsonl).
 // Device scratch (input rows + strip ring) and the staging ring are cached between calls
 // (a 2 GB stream-ordered allocation is handed back to the driver at every synchronize and
