@@ -71,6 +71,9 @@ __device__ __forceinline__ double2 bfly_fast(double2 s, double2 w, double2 c) {
     return make_double2(re, im);
 }
 
+__device__ __forceinline__ float fma_t(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ double fma_t(double a, double b, double c) { return fma(a, b, c); }
+
 template <bool EXACT, typename C> __device__ __forceinline__ C bfly(C s, C w, C c) {
     if constexpr (EXACT) return bfly_exact(s, w, c);
     else return bfly_fast(s, w, c);
