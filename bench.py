@@ -265,6 +265,15 @@ def flush_l2(buf):
     (config 2: 0.0922 -> 0.0881 ms, profiles/flush_effect_r02.jsonl)."""
     buf[0].fill_(1.0)
     buf[1].sum()
+    # ... then ~0.2 ms of device-side spinning (no memory traffic: L2 stays as flushed), so
+    # the host has certainly queued the start event and the step behind it before the device
+    # gets there.  Without it a slow host (the flush takes only ~90 us) leaves the device idle
+    # inside the interval: config 2 read 0.1065 ms instead of 0.086-0.088 on two boxes where
+    # the bench followed the test suite (profiles/c2_timing_r02.jsonl, "sleep" rows).
+    import torch
+
+    if hasattr(torch.cuda, "_sleep"):
+        torch.cuda._sleep(400000)
 
 
 def run_ours(args, cfg, rank, world, local_rank):
@@ -396,7 +405,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         "config": {"workload": cfg.name, "desc": cfg.desc, "N0": cfg.N0, "N1": cfg.N1,
                    "window": [n0, n1], "coefficients": cfg.coefficients,
                    "output_bytes": cfg.coefficients * out_bpc,
-                   "l2": "L2 flushed before every timed step: 256 MiB written, then another "
+                   "l2": "L2 flushed before every timed step (then a 0.2 ms device-side spin so host "
+                         "submission stays outside the interval): 256 MiB written, then another "
                          "256 MiB read so L2 starts clean (queued ahead of the start event, "
                          "outside the timed interval); output >> L2 as well",
                    "parallelism": (f"blocks{split[0]}x{split[1]} (window rows x window "
@@ -557,21 +567,23 @@ def other_configs(args, main_cfg, dev, flush, stream):
         e1.record(stream)
         torch.cuda.synchronize()
         reps = 5 if e0.elapsed_time(e1) > 2.0 else 25
-        for _ in range(reps):
-            torch.cuda.synchronize()
-            flush_l2(flush)  # ahead of the start event (see run_ours)
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            g.replay()
-            e1.record(stream)
-            torch.cuda.synchronize()
-            ts.append(e0.elapsed_time(e1) / 1e3)
+        with ClockSampler(dev.index or 0) as clk:
+            for _ in range(reps):
+                torch.cuda.synchronize()
+                flush_l2(flush)  # ahead of the start event (see run_ours)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                g.replay()
+                e1.record(stream)
+                torch.cuda.synchronize()
+                ts.append(e0.elapsed_time(e1) / 1e3)
         t = statistics.median(ts)
         alg = c.algorithmic_bytes(precision=pname)
         traffic = ncu_traffic(c.name, pname)
         res[name] = {"desc": c.desc, "dtype": "f32" if prec == _lib.PREC_FP32 else "f64",
                      "value": c.coefficients / t, "unit": UNIT, "kernel_ms": t * 1e3,
-                     "samples": reps,
+                     "samples": reps, "clocks": clk.summary(),
+                     "ms_min_max": [round(min(ts) * 1e3, 4), round(max(ts) * 1e3, 4)],
                      "hbm_write_gbs": c.coefficients * (16 if pname == "fp64" else 8) / t / 1e9,
                      "roofline": {"bound": "hbm", "achieved": alg / t / 1e9, "peak": peak,
                                   "unit": "GB/s", "frac": alg / t / 1e9 / peak,
