@@ -53,10 +53,6 @@
 #include "swdft2d_device.cuh"
 #include "swdft2d_internal.h"
 
-#ifndef K1_PAIR_FMA
-#define K1_PAIR_FMA 1
-#endif
-
 namespace swdft2d {
 
 #ifdef K1_TIMELINE  // tuning builds: per-CTA start / end / SM id of the last K1 launch
@@ -415,23 +411,10 @@ __global__ void __launch_bounds__(K1Shape<M0, M1, Q, TP1, NBM>::NT, MINB)
                             const C O = cur[u];
                             const int i = j + J * u;
                             const C w0 = tw[(i * sl) * ST0];
-                            if constexpr (EXACT) {
-                                const C w1 = tw[((i + (1 << (l - 1))) * sl) * ST0];
-                                cur[u] = bfly_exact(E, w0, O);
-                                cur[u + h] = bfly_exact(E, w1, O);
-                            } else {
-#if K1_PAIR_FMA
-                                // E + wO in 4 FMAs, then E - wO = 2E - (E + wO) in 2 more:
-                                // 6 FP instructions per output pair instead of 8
-                                const C a = bfly_fast(E, w0, O);
-                                cur[u] = a;
-                                cur[u + h] = mk<T>(fma_t((T)2, E.x, -a.x), fma_t((T)2, E.y, -a.y));
-#else
-                                const C t = cmul(w0, O);
-                                cur[u] = cadd(E, t);
-                                cur[u + h] = csub(E, t);
-#endif
-                            }
+                            // the node pair i, i + 2^(l-1): exact butterflies with their own
+                            // twiddles in fp64; E + wO and 2E - (E + wO) in fp32
+                            bfly_pair<EXACT>(E, w0, tw[((i + (1 << (l - 1))) * sl) * ST0], O, cur[u],
+                                             cur[u + h]);
                             rring[off + u] = O;
                         });
                     });

@@ -160,8 +160,8 @@ __global__ void __launch_bounds__(256) k2_push_kernel(const __grid_constant__ K2
             static_for<nh>([&](auto uc) {
                 constexpr int u = decltype(uc)::value;
                 const int j = t + J * u;
-                const C hi = bfly<EXACT>(sh[u], stw[(j + h) << (6 - l)], cur[u]);
-                const C lo = bfly<EXACT>(sh[u], stw[j << (6 - l)], cur[u]);
+                C lo, hi;
+                bfly_pair<EXACT>(sh[u], stw[j << (6 - l)], stw[(j + h) << (6 - l)], cur[u], lo, hi);
                 if constexpr (l < M0) {
                     cur[u + nh] = hi;
                     cur[u] = lo;

@@ -133,13 +133,11 @@ __device__ __forceinline__ void kc_pass4(const cplx<T> *src, cplx<T> *dst, const
         const C a2 = src[((p + 2 * s2) * Lt + j) * CW + col];
         const C a3 = src[((p + 3 * s2) * Lt + j) * CW + col];
         if constexpr (!HOIST) twiddles(j);
-        const C b0 = bfly<EXACT>(a0, w[0], a2), b1 = bfly<EXACT>(a0, w[1], a2);  // level t+1 at p
-        const C c0v = bfly<EXACT>(a1, w[0], a3), c1 = bfly<EXACT>(a1, w[1], a3);  // at p + s_{t+2}
-        C o[4];
-        o[0] = bfly<EXACT>(b0, w[2], c0v);
-        o[1] = bfly<EXACT>(b1, w[3], c1);
-        o[2] = bfly<EXACT>(b0, w[4], c0v);
-        o[3] = bfly<EXACT>(b1, w[5], c1);
+        C b0, b1, c0v, c1, o[4];
+        bfly_pair<EXACT>(a0, w[0], w[1], a2, b0, b1);    // level t+1 at p
+        bfly_pair<EXACT>(a1, w[0], w[1], a3, c0v, c1);   // at p + s_{t+2}
+        bfly_pair<EXACT>(b0, w[2], w[4], c0v, o[0], o[2]);
+        bfly_pair<EXACT>(b1, w[3], w[5], c1, o[1], o[3]);
         if constexpr (LAST) {
             if (col >= ncol) continue;
             const int64_t cc = c0 + col;
@@ -174,7 +172,8 @@ __device__ __forceinline__ void kc_pass2(const cplx<T> *src, cplx<T> *dst, const
     for (int it = threadIdx.x; it < items; it += KC_THREADS) {
         const int col = it % CW, p = it / CW;
         const C a0 = src[p * CW + col], a1 = src[(p + s1) * CW + col];
-        C lo = bfly<EXACT>(a0, wa, a1), hi = bfly<EXACT>(a0, wb, a1);
+        C lo, hi;
+        bfly_pair<EXACT>(a0, wa, wb, a1, lo, hi);
         if constexpr (LAST) {
             if (col >= ncol) continue;
             const int64_t cc = c0 + col;

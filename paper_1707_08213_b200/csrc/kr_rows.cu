@@ -75,7 +75,8 @@ __device__ __forceinline__ void kr_pass2(const cplx<T> *src, cplx<T> *dst, const
     for (int it = threadIdx.x; it < items; it += KR_THREADS) {
         const int p = it >> t;
         const C a0 = src[p * Lt + j], a1 = src[(p + s1) * Lt + j];
-        C lo = bfly<EXACT>(a0, wa, a1), hi = bfly<EXACT>(a0, wb, a1);
+        C lo, hi;
+        bfly_pair<EXACT>(a0, wa, wb, a1, lo, hi);
         if constexpr (LAST) {
             if (P.apply_scale) {  // uniform branch: no predicated multiplies when unscaled
                 lo = cscale(lo, f);
@@ -112,13 +113,11 @@ __device__ __forceinline__ void kr_pass4(const cplx<T> *src, cplx<T> *dst, const
         const int p = it >> t;
         const C a0 = src[p * Lt + j], a1 = src[(p + s2) * Lt + j];
         const C a2 = src[(p + 2 * s2) * Lt + j], a3 = src[(p + 3 * s2) * Lt + j];
-        const C b0 = bfly<EXACT>(a0, w1a, a2), b1 = bfly<EXACT>(a0, w1b, a2);  // level t+1 at p
-        const C c0 = bfly<EXACT>(a1, w1a, a3), c1 = bfly<EXACT>(a1, w1b, a3);  // at p + s_{t+2}
-        C o[4];
-        o[0] = bfly<EXACT>(b0, w2[0], c0);
-        o[1] = bfly<EXACT>(b1, w2[1], c1);
-        o[2] = bfly<EXACT>(b0, w2[2], c0);
-        o[3] = bfly<EXACT>(b1, w2[3], c1);
+        C b0, b1, c0, c1, o[4];
+        bfly_pair<EXACT>(a0, w1a, w1b, a2, b0, b1);  // level t+1 at p
+        bfly_pair<EXACT>(a1, w1a, w1b, a3, c0, c1);  // at p + s_{t+2}
+        bfly_pair<EXACT>(b0, w2[0], w2[2], c0, o[0], o[2]);
+        bfly_pair<EXACT>(b1, w2[1], w2[3], c1, o[1], o[3]);
         if constexpr (LAST) {
             C *d = dst + p * n + j;
             if (P.apply_scale) {  // uniform branch: no predicated multiplies when unscaled
